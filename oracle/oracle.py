@@ -1,0 +1,240 @@
+"""ctypes wrapper over oracle/liboracle.so (ozaki_ref.c + dd_ref.c).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Arrays follow the BLAS
+column-major convention: a matrix buffer is a numpy float64 array (any shape,
+Fortran/contiguous memory) addressed as ``M[i + j*ld]``.
+"""
+import ctypes as ct
+import os
+
+import numpy as np
+
+from . import build as _build
+
+_lib = None
+
+OP = {"N": 0, "T": 1, "C": 2, 0: 0, 1: 1, 2: 2}
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = _build.build()
+        L = ct.CDLL(path)
+        i64, i32, dbl, vp = ct.c_int64, ct.c_int, ct.c_double, ct.c_void_p
+        L.oz_ref_alpha.argtypes = [i32, i64]
+        L.oz_ref_alpha.restype = i32
+        L.oz_ref_bps.argtypes = [i32, i32, i64]
+        L.oz_ref_bps.restype = i32
+        L.oz_ref_slice_width.argtypes = [i64]
+        L.oz_ref_slice_width.restype = i32
+        L.oz_ref_budget_ok.argtypes = [i32, i64]
+        L.oz_ref_budget_ok.restype = i32
+        L.oz_ref_gemm_count.argtypes = [i32]
+        L.oz_ref_gemm_count.restype = i64
+        L.oz_ref_split.argtypes = [i32, i64, i64, vp, i64, i32, i32, vp, vp, vp]
+        L.oz_ref_split.restype = i32
+        L.oz_ref_int_gemm.argtypes = [i64, i64, i64, vp, vp, vp]
+        L.oz_ref_int_gemm.restype = i32
+        L.oz_ref_dgemm_sub.argtypes = [i32, i32, i64, i64, i64, dbl, vp, i64, vp, i64, dbl, vp,
+                                       i64, i32, i32, vp, i64, vp, i64]
+        L.oz_ref_dgemm_sub.restype = i32
+        L.oz_ref_level_sums_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, i32,
+                                            vp, i64, vp, i64, vp]
+        L.oz_ref_level_sums_sub.restype = i32
+        L.dd_two_sum.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
+        L.dd_two_prod.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
+        L.dd_gemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                  vp, vp]
+        L.dd_gemm_sub.restype = i32
+        L.fp64_gemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                    vp]
+        L.fp64_gemm_sub.restype = i32
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ct.c_void_p) if a is not None else None
+
+
+def _f64(a):
+    a = np.asarray(a, dtype=np.float64)
+    # keep memory order as given (column-major buffers are usually Fortran arrays)
+    if not (a.flags.f_contiguous or a.flags.c_contiguous):
+        a = np.asfortranarray(a)
+    return a
+
+
+def _idx(v, n):
+    if v is None:
+        return np.arange(n, dtype=np.int64)
+    return np.ascontiguousarray(np.asarray(v, dtype=np.int64))
+
+
+# --- A1 planner -------------------------------------------------------------
+
+def alpha(l_acc, k):
+    return lib().oz_ref_alpha(int(l_acc), int(k))
+
+
+def bps(l_in, l_acc, k):
+    return lib().oz_ref_bps(int(l_in), int(l_acc), int(k))
+
+
+def slice_width(k):
+    return lib().oz_ref_slice_width(int(k))
+
+
+def budget_ok(w, k):
+    return bool(lib().oz_ref_budget_ok(int(w), int(k)))
+
+
+def gemm_count(s):
+    return int(lib().oz_ref_gemm_count(int(s)))
+
+
+# --- A2/A3 split -------------------------------------------------------------
+
+def split(M, trans, rows, kdim, ld, s, w):
+    """Split `rows` vectors of length `kdim`: v(r,l) = M[r + l*ld] (trans 0) or
+    M[l + r*ld] (trans 1).  Returns (digits[s][rows][kdim] int8, E int32, nonfinite uint8)."""
+    M = _f64(M)
+    d = np.zeros((s, rows, kdim), dtype=np.int8)
+    E = np.zeros(rows, dtype=np.int32)
+    bad = np.zeros(rows, dtype=np.uint8)
+    rc = lib().oz_ref_split(int(trans), rows, kdim, _p(M), int(ld), int(s), int(w), _p(d), _p(E),
+                            _p(bad))
+    if rc:
+        raise ValueError(f"oz_ref_split failed rc={rc}")
+    return d, E, bad
+
+
+def split_opA(A, transA, m, k, lda, s, w=None):
+    """Rows of op(A) (m x k)."""
+    w = slice_width(k) if w is None else w
+    return split(A, 0 if OP[transA] == 0 else 1, m, k, lda, s, w)
+
+
+def split_opB(B, transB, k, n, ldb, s, w=None):
+    """Columns of op(B) (k x n), returned as digits[s][n][k]."""
+    w = slice_width(k) if w is None else w
+    return split(B, 1 if OP[transB] == 0 else 0, n, k, ldb, s, w)
+
+
+# --- A4 -------------------------------------------------------------------------
+
+def int_gemm(a, b):
+    """a: [ra][k] int8, b: [rb][k] int8 (columns of op(B)) -> [ra][rb] int32."""
+    a = np.ascontiguousarray(a, dtype=np.int8)
+    b = np.ascontiguousarray(b, dtype=np.int8)
+    ra, k = a.shape
+    rb, k2 = b.shape
+    assert k == k2
+    P = np.zeros((ra, rb), dtype=np.int32)
+    rc = lib().oz_ref_int_gemm(ra, rb, k, _p(a), _p(b), _p(P))
+    if rc:
+        raise OverflowError("INT32 partial sum overflow")
+    return P
+
+
+# --- A5 full method -------------------------------------------------------------
+
+def dgemm(transA, transB, m, n, k, alpha_, A, lda, B, ldb, beta, C, ldc, s, mode="L",
+          rows=None, cols=None):
+    """Ozaki-scheme DGEMM.  Returns a copy of C (same buffer layout) with the
+    selected rows x cols block overwritten.  mode 'L' = canonical level order
+    (parity target), 'P' = paper-literal Alg. 3 order."""
+    A = _f64(A)
+    B = _f64(B)
+    Cout = np.array(C, dtype=np.float64, copy=True, order="K")
+    ri, cj = _idx(rows, m), _idx(cols, n)
+    rc = lib().oz_ref_dgemm_sub(OP[transA], OP[transB], m, n, k, float(alpha_), _p(A), lda,
+                                _p(B), ldb, float(beta), _p(Cout), ldc, int(s),
+                                0 if mode == "L" else 1, _p(ri), len(ri), _p(cj), len(cj))
+    if rc:
+        raise ValueError(f"oz_ref_dgemm_sub failed rc={rc}")
+    return Cout
+
+
+def dgemm_simple(A, B, s, mode="L", alpha_=1.0, beta=0.0, C=None, transA="N", transB="N",
+                 rows=None, cols=None):
+    """Convenience: A, B numpy 2-D arrays holding the *stored* matrices
+    (column-major semantics via Fortran order)."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    B = np.asfortranarray(B, dtype=np.float64)
+    m = A.shape[0] if OP[transA] == 0 else A.shape[1]
+    k = A.shape[1] if OP[transA] == 0 else A.shape[0]
+    n = B.shape[1] if OP[transB] == 0 else B.shape[0]
+    if C is None:
+        C = np.zeros((m, n), dtype=np.float64, order="F")
+    C = np.asfortranarray(C, dtype=np.float64)
+    return dgemm(transA, transB, m, n, k, alpha_, A, A.shape[0], B, B.shape[0], beta, C, m, s,
+                 mode, rows, cols)
+
+
+def level_sums(transA, transB, m, n, k, A, lda, B, ldb, s, rows=None, cols=None):
+    """Exact level sums L_g (g = 2..s+1) -> int64 [s][nr][nc]."""
+    A = _f64(A)
+    B = _f64(B)
+    ri, cj = _idx(rows, m), _idx(cols, n)
+    out = np.zeros((s, len(ri), len(cj)), dtype=np.int64)
+    rc = lib().oz_ref_level_sums_sub(OP[transA], OP[transB], m, n, k, _p(A), lda, _p(B), ldb,
+                                     int(s), _p(ri), len(ri), _p(cj), len(cj), _p(out))
+    if rc:
+        raise ValueError(f"oz_ref_level_sums_sub failed rc={rc}")
+    return out
+
+
+# --- DD reference ------------------------------------------------------------------
+
+def two_sum(a, b):
+    hi, lo = ct.c_double(), ct.c_double()
+    lib().dd_two_sum(float(a), float(b), ct.byref(hi), ct.byref(lo))
+    return hi.value, lo.value
+
+
+def two_prod(a, b):
+    hi, lo = ct.c_double(), ct.c_double()
+    lib().dd_two_prod(float(a), float(b), ct.byref(hi), ct.byref(lo))
+    return hi.value, lo.value
+
+
+def dd_gemm(transA, transB, m, n, k, A, lda, B, ldb, rows=None, cols=None):
+    """Returns (hi, lo) as [nr][nc] arrays."""
+    A = _f64(A)
+    B = _f64(B)
+    ri, cj = _idx(rows, m), _idx(cols, n)
+    hi = np.zeros((len(ri), len(cj)))
+    lo = np.zeros((len(ri), len(cj)))
+    lib().dd_gemm_sub(OP[transA], OP[transB], m, n, k, _p(A), lda, _p(B), ldb, _p(ri), len(ri),
+                      _p(cj), len(cj), _p(hi), _p(lo))
+    return hi, lo
+
+
+def fp64_gemm(transA, transB, m, n, k, A, lda, B, ldb, rows=None, cols=None):
+    A = _f64(A)
+    B = _f64(B)
+    ri, cj = _idx(rows, m), _idx(cols, n)
+    out = np.zeros((len(ri), len(cj)))
+    lib().fp64_gemm_sub(OP[transA], OP[transB], m, n, k, _p(A), lda, _p(B), ldb, _p(ri),
+                        len(ri), _p(cj), len(cj), _p(out))
+    return out
+
+
+def err_stats(C, hi, lo):
+    """Relative error of C vs the DD reference: per element
+    |C - C_DD| / |C_DD| with C_DD = hi + lo; entries with C_DD == 0 excluded
+    (counted).  Returns dict(mean_rel, max_rel, nw_max, zero_ref).
+    nw_max = max|C - C_DD| / max|C_DD| (normwise reading)."""
+    C = np.asarray(C, dtype=np.float64)
+    diff = np.abs((C - hi) - lo)
+    ref = np.abs(hi)
+    nz = ref != 0
+    rel = diff[nz] / ref[nz]
+    return {
+        "mean_rel": float(rel.mean()) if rel.size else 0.0,
+        "max_rel": float(rel.max()) if rel.size else 0.0,
+        "nw_max": float(diff.max() / ref.max()) if ref.max() > 0 else float(diff.max()),
+        "zero_ref": int((~nz).sum()),
+    }

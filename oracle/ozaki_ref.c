@@ -1,0 +1,329 @@
+/*
+ * oracle/ozaki_ref.c -- CPU ORACLE for the Ozaki scheme on integer matrix units
+ * (Ootomo, Ozaki, Yokota, arXiv 2306.11975).
+ *
+ * *** TEST INFRASTRUCTURE ONLY. ***
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load this library.  The product path (libozimmu.so and the
+ * paper_2306_11975_b200 package) never links, imports or calls it, and this file
+ * shares no code, header, table or helper with the CUDA path.
+ *
+ * It is a plain, slow, obviously-correct restatement of the paper's algorithm in
+ * the paper's order and notation.  Citations are "P:<line>" into PAPER.md and
+ * name the section / algorithm / equation.  Where the paper is silent or garbled
+ * the reading taken is the one listed in SURVEY.md s8(c) and DESIGN.md s3
+ * ("reading A<n>").
+ *
+ * Build: gcc -std=c99 -O2 -fopenmp -ffp-contract=off -fPIC -shared  (no -ffast-math:
+ * every floating-point operation below is an IEEE-754 binary64 operation with
+ * round-to-nearest-even, and the order of operations is the order written).
+ *
+ * Layout conventions (BLAS, column-major):
+ *   op(A) is m x k, op(A)(i,l) = transA==0 ? A[i + l*lda] : A[l + i*lda]
+ *   op(B) is k x n, op(B)(l,j) = transB==0 ? B[l + j*ldb] : B[j + l*ldb]
+ *   C     is m x n, C(i,j)    = C[i + j*ldc]
+ * (trans codes: 0 = N, 1 = T, 2 = C; C is identical to T for real data.)
+ *
+ * Pins: see tests/test_oracle_*.py.  Every function below is pinned by a test
+ * against something other than itself (SPEC/paper worked examples, exact
+ * rational arithmetic, big-integer brute force, closed forms, invariants).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OZR_OK 0
+#define OZR_ERR_ARG 1
+#define OZR_ERR_BUDGET 2   /* k * (2^w - 1)^2 exceeds INT32 (would break exactness) */
+#define OZR_ERR_OVERFLOW 3 /* an INT32 partial product left the INT32 range (must never happen) */
+
+/* ------------------------------------------------------------------------- */
+/* A1: slice width.                                                           */
+/* ------------------------------------------------------------------------- */
+
+/* Eq. alpha (s2.3.1) in the integer-unit form of s3.2.1:
+ *     alpha = floor((l_acc - log2 k) / 2)
+ * with l_acc the accumulator mantissa length (31 for INT32, Table 2).
+ * The real-valued log2 is used exactly as printed. */
+int oz_ref_alpha(int l_acc, int64_t k)
+{
+    return (int)floor(((double)l_acc - log2((double)k)) / 2.0);
+}
+
+/* BPS = min(alpha, l_in) (s3.2.1); for INT8-INT32, l_in = 7, l_acc = 31
+ * (Table 2).  Returns <= 0 when no exact accumulation is possible. */
+int oz_ref_bps(int l_in, int l_acc, int64_t k)
+{
+    int a = oz_ref_alpha(l_acc, k);
+    return a < l_in ? a : l_in;
+}
+
+/* Slice width used by the method on INT8-INT32 (reading A2: the positional
+ * scale of Alg. 3 line 7 uses w = BPS, not alpha). */
+int oz_ref_slice_width(int64_t k)
+{
+    return oz_ref_bps(7, 31, k);
+}
+
+/* No-overflow budget ("absence of rounding errors ... absence of
+ * overflow"): k products of two w-bit magnitudes must fit in INT32. */
+int oz_ref_budget_ok(int w, int64_t k)
+{
+    int64_t d = ((int64_t)1 << w) - 1;
+    return (double)k * (double)(d * d) <= 2147483647.0;
+}
+
+/* #GEMM = s(s+1)/2 (s3.2.4): pairs with i + j <= s + 1. */
+int64_t oz_ref_gemm_count(int s)
+{
+    return (int64_t)s * (s + 1) / 2;
+}
+
+/* ------------------------------------------------------------------------- */
+/* A2 + A3: SplitInt (Alg. 4).                                     */
+/* ------------------------------------------------------------------------- */
+
+/* Split `rows` vectors of length `kdim`; vector r, element l is
+ *     v(r,l) = trans==0 ? M[r + l*ld] : M[l + r*ld].
+ * For op(A) call with trans = transA; for the columns of op(B) call with
+ * trans = !transB (column j of op(B) is row j of op(B)^T).
+ *
+ * Alg. 4 line 2 (reading A3): e_r = 2^E_r with E_r the frexp exponent of
+ * max_l |v(r,l)|, so that |v| / 2^E_r < 1 strictly; E_r = 0 for an all-zero row.
+ * Alg. 4 lines 3-5 (readings A4, A5): slice p (p = 1..s) of v holds, with the
+ * sign of v, the bits of |v| / 2^E_r at positions (p-1)w+1 .. pw after the
+ * binary point:
+ *     d_p = sgn(v) * ( floor( |v| * 2^(w p - E_r) ) mod 2^w ).
+ * Each digit is computed from |v| with ONE ldexp (exact: the result is either
+ * >= 1, hence normal, or < 1 where floor gives 0 regardless of rounding),
+ * then floor and fmod, all exact in binary64.
+ * Reading A9: a row containing a NaN or Inf gets nonfinite[r] = 1 and zero
+ * digits; the final result is NaN for every output in that row / column.
+ *
+ * digits: int8 array [s][rows][kdim] (digit p of v(r,l) at ((p-1)*rows + r)*kdim + l).
+ * E:      int32 [rows];  nonfinite: uint8 [rows] (may be NULL). */
+int oz_ref_split(int trans, int64_t rows, int64_t kdim, const double *M, int64_t ld,
+                 int s, int w, int8_t *digits, int32_t *E, uint8_t *nonfinite)
+{
+    if (rows < 0 || kdim < 0 || s < 1 || w < 1 || w > 7) return OZR_ERR_ARG;
+    const double two_w = ldexp(1.0, w);
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r) {
+        double vmax = 0.0;
+        int bad = 0;
+        for (int64_t l = 0; l < kdim; ++l) {
+            double v = trans == 0 ? M[r + l * ld] : M[l + r * ld];
+            if (!isfinite(v)) bad = 1;
+            else if (fabs(v) > vmax) vmax = fabs(v);
+        }
+        int Er = 0;
+        if (vmax != 0.0) (void)frexp(vmax, &Er); /* vmax = f * 2^Er, f in [0.5, 1) */
+        if (bad) Er = 0;
+        E[r] = Er;
+        if (nonfinite) nonfinite[r] = (uint8_t)bad;
+        for (int p = 1; p <= s; ++p) {
+            int8_t *dp = digits + ((int64_t)(p - 1) * rows + r) * kdim;
+            for (int64_t l = 0; l < kdim; ++l) {
+                double v = trans == 0 ? M[r + l * ld] : M[l + r * ld];
+                if (bad || v == 0.0) { dp[l] = 0; continue; }
+                double t = floor(ldexp(fabs(v), w * p - Er));
+                double d = fmod(t, two_w);           /* in [0, 2^w - 1] */
+                dp[l] = (int8_t)(v < 0.0 ? -d : d);
+            }
+        }
+    }
+    return OZR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* A4: one INT8 x INT8 -> INT32 slice product (Alg. 3 line 6).         */
+/* ------------------------------------------------------------------------- */
+
+/* P(i,j) = sum_l a(i,l) * b(j,l) where a is [ra][kdim] and b is [rb][kdim]
+ * (b holds the columns of op(B)).  The sum is formed in int64 and checked to
+ * lie in INT32 at every partial step -- that check IS the paper's claim that
+ * the integer GEMM is error-free.  Output P is [ra][rb] row-major
+ * INT32.  Returns OZR_ERR_OVERFLOW if any partial sum leaves INT32. */
+int oz_ref_int_gemm(int64_t ra, int64_t rb, int64_t kdim, const int8_t *a,
+                    const int8_t *b, int32_t *P)
+{
+    int err = 0;
+#pragma omp parallel for schedule(static) reduction(| : err)
+    for (int64_t i = 0; i < ra; ++i) {
+        for (int64_t j = 0; j < rb; ++j) {
+            int64_t acc = 0;
+            for (int64_t l = 0; l < kdim; ++l) {
+                acc += (int64_t)a[i * kdim + l] * (int64_t)b[j * kdim + l];
+                if (acc > INT32_MAX || acc < INT32_MIN) err = 1;
+            }
+            P[i * rb + j] = (int32_t)acc;
+        }
+    }
+    return err ? OZR_ERR_OVERFLOW : OZR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* A5: accumulation and output (Alg. 3 line 7), readings A6-A9.         */
+/* ------------------------------------------------------------------------- */
+
+/* Result of the split + pair products for a block of output elements: the exact
+ * level sums L_g = sum_{p+q=g} P_pq (g = 2..s+1), in int64 (exact: |L_g| <=
+ * s k (2^w-1)^2 < 2^53).  Stored as Lg[(g-2)][i][j], i over the `nr` selected
+ * rows, j over the `nc` selected columns (row-major within a level). */
+static int level_sums(int s, int64_t nr, int64_t nc, int64_t kdim,
+                      const int8_t *dA, const int8_t *dB, int64_t *Lg)
+{
+    int err = 0;
+    int32_t *P = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nr * nc > 0 ? nr * nc : 1));
+    if (!P) return OZR_ERR_ARG;
+    memset(Lg, 0, sizeof(int64_t) * (size_t)(s * nr * nc));
+    /* Alg. 3 lines 4-6: i = 1..s, j = 1..(s - i + 1). */
+    for (int p = 1; p <= s; ++p) {
+        for (int q = 1; q <= s - p + 1; ++q) {
+            int e = oz_ref_int_gemm(nr, nc, kdim, dA + (int64_t)(p - 1) * nr * kdim,
+                                    dB + (int64_t)(q - 1) * nc * kdim, P);
+            if (e) err = e;
+            int64_t *L = Lg + (int64_t)(p + q - 2) * nr * nc;
+            for (int64_t t = 0; t < nr * nc; ++t) L[t] += P[t];
+        }
+    }
+    free(P);
+    return err;
+}
+
+/* Reading A8 (BLAS semantics, alpha/beta not in the paper):
+ *   alpha == 0          : C = beta * C_in          (C = 0 when beta == 0)
+ *   beta  == 0          : C = alpha * X            (C_in never read)
+ *   otherwise           : C = fma(alpha, X, beta * C_in)  with beta*C_in rounded first. */
+static double apply_alpha_beta(double alpha, double X, double beta, double cin)
+{
+    if (beta == 0.0) return alpha * X;
+    return fma(alpha, X, beta * cin);
+}
+
+/* Full method for the sub-block of C given by row indices `ri` (nr of them)
+ * and column indices `cj` (nc of them).  Writes C[ri[a] + cj[b]*ldc] only.
+ * mode 0 = canonical order (reading A6, "mode L"): exact level sums, then
+ *          acc = +0; for g = s+1 down to 2: acc = acc + L_g * 2^(-w g)
+ *          (one rounding per add; the product is exact);
+ * mode 1 = paper-literal Alg. 3 order ("mode P"): for i = 1..s, for
+ *          j = 1..s-i+1: acc = acc + P_ij * 2^(-w(i+j))  (accuracy comparison only).
+ * Then (reading A7) X = ldexp(acc, E_A[i] + E_B[j]) -- one ldexp, i.e. one
+ * correctly-rounded scaling, applied once -- and reading A8 for alpha/beta.
+ * Reading A9: non-finite input in row i of op(A) or column j of op(B) -> X = NaN. */
+int oz_ref_dgemm_sub(int transA, int transB, int64_t m, int64_t n, int64_t k,
+                     double alpha, const double *A, int64_t lda, const double *B,
+                     int64_t ldb, double beta, double *C, int64_t ldc, int s, int mode,
+                     const int64_t *ri, int64_t nr, const int64_t *cj, int64_t nc)
+{
+    if (m < 0 || n < 0 || k < 0 || s < 1 || nr < 0 || nc < 0) return OZR_ERR_ARG;
+    if (nr == 0 || nc == 0) return OZR_OK;
+    for (int64_t a = 0; a < nr; ++a) if (ri[a] < 0 || ri[a] >= m) return OZR_ERR_ARG;
+    for (int64_t b = 0; b < nc; ++b) if (cj[b] < 0 || cj[b] >= n) return OZR_ERR_ARG;
+
+    if (alpha == 0.0 || k == 0) {           /* A and B are not read (BLAS quick return) */
+        for (int64_t b = 0; b < nc; ++b)
+            for (int64_t a = 0; a < nr; ++a) {
+                double *c = &C[ri[a] + cj[b] * ldc];
+                *c = beta == 0.0 ? 0.0 : beta * *c;
+            }
+        return OZR_OK;
+    }
+    int w = oz_ref_slice_width(k);
+    if (w < 1 || !oz_ref_budget_ok(w, k)) return OZR_ERR_BUDGET;
+
+    /* Gather the selected rows of op(A) and columns of op(B) into dense
+     * row-vector form, then split them (Alg. 3 lines 1-2). */
+    double *Ar = (double *)malloc(sizeof(double) * (size_t)(nr * k));
+    double *Bc = (double *)malloc(sizeof(double) * (size_t)(nc * k));
+    int8_t *dA = (int8_t *)malloc((size_t)(s * nr * k));
+    int8_t *dB = (int8_t *)malloc((size_t)(s * nc * k));
+    int32_t *EA = (int32_t *)malloc(sizeof(int32_t) * (size_t)nr);
+    int32_t *EB = (int32_t *)malloc(sizeof(int32_t) * (size_t)nc);
+    uint8_t *bA = (uint8_t *)malloc((size_t)nr), *bB = (uint8_t *)malloc((size_t)nc);
+    int64_t *Lg = (int64_t *)malloc(sizeof(int64_t) * (size_t)(s * nr * nc));
+    int32_t *P = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nr * nc));
+    int err = OZR_OK;
+    if (!Ar || !Bc || !dA || !dB || !EA || !EB || !bA || !bB || !Lg || !P) { err = OZR_ERR_ARG; goto done; }
+    for (int64_t a = 0; a < nr; ++a)
+        for (int64_t l = 0; l < k; ++l)
+            Ar[a * k + l] = transA == 0 ? A[ri[a] + l * lda] : A[l + ri[a] * lda];
+    for (int64_t b = 0; b < nc; ++b)
+        for (int64_t l = 0; l < k; ++l)
+            Bc[b * k + l] = transB == 0 ? B[l + cj[b] * ldb] : B[cj[b] + l * ldb];
+    /* Ar / Bc are row-major [n][k]: row r element l at r*k + l, i.e. trans=1, ld=k. */
+    if ((err = oz_ref_split(1, nr, k, Ar, k, s, w, dA, EA, bA))) goto done;
+    if ((err = oz_ref_split(1, nc, k, Bc, k, s, w, dB, EB, bB))) goto done;
+
+    if (mode == 0) {
+        if ((err = level_sums(s, nr, nc, k, dA, dB, Lg))) goto done;
+#pragma omp parallel for schedule(static)
+        for (int64_t a = 0; a < nr; ++a)
+            for (int64_t b = 0; b < nc; ++b) {
+                double acc = 0.0;
+                for (int g = s + 1; g >= 2; --g) {
+                    double term = (double)Lg[(int64_t)(g - 2) * nr * nc + a * nc + b] * ldexp(1.0, -w * g);
+                    acc = acc + term;
+                }
+                double X = (bA[a] || bB[b]) ? NAN : ldexp(acc, EA[a] + EB[b]);
+                double *c = &C[ri[a] + cj[b] * ldc];
+                *c = apply_alpha_beta(alpha, X, beta, beta == 0.0 ? 0.0 : *c);
+            }
+    } else {
+        double *acc = (double *)calloc((size_t)(nr * nc), sizeof(double));
+        if (!acc) { err = OZR_ERR_ARG; goto done; }
+        for (int p = 1; p <= s && !err; ++p)
+            for (int q = 1; q <= s - p + 1; ++q) {
+                int e = oz_ref_int_gemm(nr, nc, k, dA + (int64_t)(p - 1) * nr * k,
+                                        dB + (int64_t)(q - 1) * nc * k, P);
+                if (e) { err = e; break; }
+                double sc = ldexp(1.0, -w * (p + q));
+                for (int64_t t = 0; t < nr * nc; ++t) acc[t] = acc[t] + (double)P[t] * sc;
+            }
+        if (!err)
+            for (int64_t a = 0; a < nr; ++a)
+                for (int64_t b = 0; b < nc; ++b) {
+                    double X = (bA[a] || bB[b]) ? NAN : ldexp(acc[a * nc + b], EA[a] + EB[b]);
+                    double *c = &C[ri[a] + cj[b] * ldc];
+                    *c = apply_alpha_beta(alpha, X, beta, beta == 0.0 ? 0.0 : *c);
+                }
+        free(acc);
+    }
+done:
+    free(Ar); free(Bc); free(dA); free(dB); free(EA); free(EB); free(bA); free(bB); free(Lg); free(P);
+    return err;
+}
+
+/* Exact level sums for a sub-block (test hook for the GPU's
+ * ozimmu_debug_level_sums).  Lg_out: int64 [s][nr][nc] row-major, level g at
+ * index g-2. */
+int oz_ref_level_sums_sub(int transA, int transB, int64_t m, int64_t n, int64_t k,
+                          const double *A, int64_t lda, const double *B, int64_t ldb,
+                          int s, const int64_t *ri, int64_t nr, const int64_t *cj,
+                          int64_t nc, int64_t *Lg_out)
+{
+    if (m < 0 || n < 0 || k < 1 || s < 1 || nr < 1 || nc < 1) return OZR_ERR_ARG;
+    int w = oz_ref_slice_width(k);
+    if (w < 1 || !oz_ref_budget_ok(w, k)) return OZR_ERR_BUDGET;
+    double *Ar = (double *)malloc(sizeof(double) * (size_t)(nr * k));
+    double *Bc = (double *)malloc(sizeof(double) * (size_t)(nc * k));
+    int8_t *dA = (int8_t *)malloc((size_t)(s * nr * k));
+    int8_t *dB = (int8_t *)malloc((size_t)(s * nc * k));
+    int32_t *EA = (int32_t *)malloc(sizeof(int32_t) * (size_t)nr);
+    int32_t *EB = (int32_t *)malloc(sizeof(int32_t) * (size_t)nc);
+    int err = OZR_ERR_ARG;
+    if (Ar && Bc && dA && dB && EA && EB) {
+        for (int64_t a = 0; a < nr; ++a)
+            for (int64_t l = 0; l < k; ++l)
+                Ar[a * k + l] = transA == 0 ? A[ri[a] + l * lda] : A[l + ri[a] * lda];
+        for (int64_t b = 0; b < nc; ++b)
+            for (int64_t l = 0; l < k; ++l)
+                Bc[b * k + l] = transB == 0 ? B[l + cj[b] * ldb] : B[cj[b] + l * ldb];
+        err = oz_ref_split(1, nr, k, Ar, k, s, w, dA, EA, NULL);
+        if (!err) err = oz_ref_split(1, nc, k, Bc, k, s, w, dB, EB, NULL);
+        if (!err) err = level_sums(s, nr, nc, k, dA, dB, Lg_out);
+    }
+    free(Ar); free(Bc); free(dA); free(dB); free(EA); free(EB);
+    return err;
+}
