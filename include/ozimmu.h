@@ -1,0 +1,176 @@
+/*
+ * ozimmu.h -- C ABI of the B200-native Ozaki-scheme DGEMM on INT8 tensor cores.
+ *
+ * Method: Ootomo, Ozaki, Yokota, "DGEMM on Integer Matrix Multiplication Unit",
+ * arXiv 2306.11975.  Citations "P:<line>" refer to that paper's text
+ * (PAPER.md), with section / algorithm / equation.
+ *
+ *   C = alpha * op(A) * op(B) + beta * C          (BLAS DGEMM semantics)
+ *
+ * computed as
+ *   A1  w = min(7, floor((31 - log2 k)/2))                     Eq. alpha, BPS P:457-460
+ *   A2  E_A[i] = frexp exponent of max_l |op(A)(i,l)|,  E_B[j] likewise per column of op(B)
+ *                                                              Alg. 4 line 2, P:394 (reading A3)
+ *   A3  digits d_p = sgn(x) * (floor(|x| 2^(wp - E)) mod 2^w), p = 1..s,  INT8
+ *                                                              Alg. 4 lines 3-5, P:396-401 (A4, A5)
+ *   A4  P_pq = A^(p) * B^(q)  (INT8 x INT8 -> INT32, exact) for p + q <= s + 1
+ *                                                              Alg. 3 line 6
+ *   A5  L_g = sum_{p+q=g} P_pq (exact);  acc = +0;  for g = s+1 down to 2: acc += L_g 2^(-wg);
+ *       X = ldexp(acc, E_A[i] + E_B[j]);  C = alpha X (+ beta C)  Alg. 3 line 7, P:382 (A6-A8)
+ * on sm_100a: A2/A3 by a slicing kernel, A4+A5 by one persistent tcgen05 kernel
+ * (TMA -> SMEM, tcgen05.mma.kind::i8 into TMEM, fused FP64 epilogue).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Column-major matrices (cuBLAS convention).  Element (i, j) of a matrix X
+ *    with leading dimension ldX is X[i + j*ldX].  For row-major (e.g. torch)
+ *    tensors call with swapped operands: C^T = B^T A^T; the result is bitwise
+ *    the same because the exponent assignment is symmetric.
+ *  - A, B, C and the workspace are DEVICE pointers owned by the caller.
+ *    alpha and beta are HOST pointers.  Nothing is freed by the library except
+ *    the internal workspace it allocated itself.
+ *  - Every computing call is asynchronous on the handle's stream (default: the
+ *    legacy default stream); it never synchronises the device.  Argument errors
+ *    are detected synchronously and returned before anything is launched;
+ *    launch failures are returned as OZIMMU_ERR_CUDA (asynchronous execution
+ *    errors surface at the caller's next synchronisation).
+ *  - Quick returns (BLAS): m == 0 or n == 0 -> no-op; alpha == 0 or k == 0 ->
+ *    C = beta*C without reading A or B; beta == 0 -> C is not read (NaN in C is
+ *    ignored).
+ *  - num_slices = s in [1, OZIMMU_MAX_SLICES].  0 (the paper's INT8-AUTO,
+ *    P:656-659) is reserved and returns OZIMMU_ERR_UNSUPPORTED.
+ *  - k is limited to OZIMMU_MAX_K (w >= 5); larger k returns OZIMMU_ERR_UNSUPPORTED.
+ *  - Non-finite inputs (reading A9): if row i of op(A) or column j of op(B)
+ *    contains NaN/Inf, C(i,j) = NaN (for alpha != 0).  No error is returned.
+ *  - Results are deterministic and independent of the launch configuration,
+ *    the stream, the device and the row/column partitioning.
+ */
+#ifndef OZIMMU_H
+#define OZIMMU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define OZIMMU_API __attribute__((visibility("default")))
+#else
+#define OZIMMU_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OZIMMU_MAX_SLICES 32
+#define OZIMMU_MAX_K (1LL << 21)
+
+typedef struct ozimmu_ctx *ozimmu_handle_t;
+
+typedef enum { OZIMMU_OP_N = 0, OZIMMU_OP_T = 1, OZIMMU_OP_C = 2 } ozimmu_op_t;
+
+typedef enum {
+    OZIMMU_SUCCESS = 0,
+    OZIMMU_ERR_INVALID_VALUE = 1, /* bad argument (negative size, ld too small, NULL, bad s) */
+    OZIMMU_ERR_UNSUPPORTED = 2,   /* valid BLAS call outside what is implemented (s = 0, k too large) */
+    OZIMMU_ERR_WORKSPACE = 3,     /* caller workspace too small / allocation failed */
+    OZIMMU_ERR_CUDA = 4,          /* a CUDA runtime/driver call or launch failed */
+    OZIMMU_ERR_NOT_INITIALIZED = 5
+} ozimmu_status_t;
+
+/* Per-call report of the last computing call on a handle (SPEC GemmReport, S:378-381;
+ * the paper's time-breakdown phases). */
+typedef struct {
+    int num_slices;        /* s */
+    int slice_width;       /* w (bits per slice, BPS) */
+    int64_t gemm_pairs;    /* s(s+1)/2 INT8 GEMMs */
+    int64_t int8_macs;     /* s(s+1)/2 * m * n * k */
+    int64_t slice_bytes;   /* INT8 planes + exponents written by the slicing kernels */
+    int tile_n;            /* output columns per CTA tile (TMEM-bounded) */
+    int k_block;           /* K bytes per pipeline stage */
+    int stages;            /* SMEM pipeline depth */
+    int k_chunks;          /* INT32-overflow-safe K chunks per tile (A4 budget) */
+    int launches;          /* kernels launched by the last call */
+} ozimmu_report_t;
+
+/* ---- handle ------------------------------------------------------------- */
+
+/* Create a handle bound to CUDA device `device`.  Errors: INVALID_VALUE (h NULL),
+ * CUDA (no such device / device is not sm_100). */
+OZIMMU_API ozimmu_status_t ozimmu_create(ozimmu_handle_t *h, int device);
+/* Free the internal workspace (if any) and the handle.  NULL is a no-op. */
+OZIMMU_API ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h);
+/* Set the stream (a cudaStream_t passed as void*); NULL = legacy default stream. */
+OZIMMU_API ozimmu_status_t ozimmu_set_stream(ozimmu_handle_t h, void *stream);
+/* Bytes of device workspace ozimmu_dgemm needs for this shape (0 on invalid input).
+ * = s*(m + n)*round_up(k,16) INT8 planes + 4(m+n) exponents + K-chunk scratch + alignment
+ * (the paper's working-memory cost). */
+OZIMMU_API size_t ozimmu_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m, int64_t n,
+                              int64_t k, int num_slices);
+/* Give the handle a caller-owned device workspace (256-byte aligned).  Calls whose
+ * need exceeds `bytes` return OZIMMU_ERR_WORKSPACE.  dptr = NULL reverts to the
+ * internal, lazily grown cudaMalloc workspace. */
+OZIMMU_API ozimmu_status_t ozimmu_set_workspace(ozimmu_handle_t h, void *dptr, size_t bytes);
+/* Copy the report of the last computing call. */
+OZIMMU_API ozimmu_status_t ozimmu_get_report(ozimmu_handle_t h, ozimmu_report_t *out);
+/* Library version (major*10000 + minor*100 + patch). */
+OZIMMU_API int ozimmu_version(void);
+/* Human-readable status name (static string). */
+OZIMMU_API const char *ozimmu_status_string(ozimmu_status_t s);
+
+/* ---- the method ------------------------------------------------------------ */
+
+/* C = alpha op(A) op(B) + beta C with s = num_slices INT8 slices (Alg. 3).
+ * op(A) is m x k, op(B) is k x n, C is m x n.  lda >= max(1, rows of stored A),
+ * ldb likewise, ldc >= max(1, m).  OZIMMU_OP_C equals OZIMMU_OP_T for real data. */
+OZIMMU_API ozimmu_status_t ozimmu_dgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB,
+                             int64_t m, int64_t n, int64_t k, const double *alpha,
+                             const double *A, int64_t lda, const double *B, int64_t ldb,
+                             const double *beta, double *C, int64_t ldc, int num_slices);
+
+/* ---- split-phase entry points (multi-GPU: slice B once, broadcast, reuse) -----
+ * A "B-slice buffer" is one contiguous device buffer holding the INT8 planes of
+ * the columns of op(B) plus their int32 exponents, in the exact layout the GEMM
+ * kernel reads (so it can be moved between GPUs as plain bytes, e.g. one NCCL
+ * broadcast over NVLink -- SURVEY s8e).  Its size depends only on (n, k, s). */
+OZIMMU_API size_t ozimmu_b_slices_bytes(int64_t n, int64_t k, int num_slices);
+/* Slice op(B) (k x n) into b_slices (device, ozimmu_b_slices_bytes bytes,
+ * 256-byte aligned).  Alg. 4 applied to the columns of op(B). */
+OZIMMU_API ozimmu_status_t ozimmu_slice_b(ozimmu_handle_t h, ozimmu_op_t transB, int64_t k, int64_t n,
+                               const double *B, int64_t ldb, int num_slices, void *b_slices);
+/* As ozimmu_dgemm, with op(B) given as a B-slice buffer produced by ozimmu_slice_b
+ * for the same (k, n, num_slices).  Workspace need: ozimmu_workspace_bytes(.., n=0, ..). */
+OZIMMU_API ozimmu_status_t ozimmu_dgemm_presliced_b(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m,
+                                         int64_t n, int64_t k, const double *alpha,
+                                         const double *A, int64_t lda, const void *b_slices,
+                                         const double *beta, double *C, int64_t ldc,
+                                         int num_slices);
+
+/* ---- debug / parity exports (same kernels as the product path) -------------- */
+
+/* Slices and exponents of the rows of op(M) (is_rows = 1: M is the A operand,
+ * op(M) is rows x kdim) or of the columns of op(M) (is_rows = 0: M is the B
+ * operand, op(M) is kdim x rows).  planes_out: device int8 [s][rows][kdim]
+ * (digit p of vector r, element l at ((p-1)*rows + r)*kdim + l);
+ * exps_out: device int32 [rows]; a vector holding NaN/Inf gets exponent
+ * OZIMMU_EXP_NONFINITE and zero digits. */
+#define OZIMMU_EXP_NONFINITE 0x7fffffff
+OZIMMU_API ozimmu_status_t ozimmu_debug_split(ozimmu_handle_t h, ozimmu_op_t op, int is_rows, int64_t rows,
+                                   int64_t kdim, const double *M, int64_t ld, int num_slices,
+                                   int8_t *planes_out, int32_t *exps_out);
+/* Exact level sums L_g, g = 2..s+1, computed by the tcgen05 GEMM kernel:
+ * Lg_out: device int64 [s][n][m] (level g at (g-2)*m*n + i + j*m). */
+OZIMMU_API ozimmu_status_t ozimmu_debug_level_sums(ozimmu_handle_t h, ozimmu_op_t transA,
+                                        ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                        const double *A, int64_t lda, const double *B,
+                                        int64_t ldb, int num_slices, int64_t *Lg_out);
+/* One INT8 x INT8 -> INT32 product P = Ai * Bj^T on the tcgen05 kernel.
+ * Ai: device int8 [m][k] (row i contiguous), Bj: device int8 [n][k] (column j of
+ * the right operand contiguous), P_out: device int32 [n][m] (P(i,j) at i + j*m).
+ * Requires k * max|Ai| * max|Bj| <= 2^31 - 1 (caller's responsibility). */
+OZIMMU_API ozimmu_status_t ozimmu_debug_pair(ozimmu_handle_t h, const int8_t *Ai, const int8_t *Bj,
+                                  int64_t m, int64_t n, int64_t k, int32_t *P_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZIMMU_H */

@@ -1,0 +1,11 @@
+"""B200-native Ozaki-scheme DGEMM on INT8 tensor cores (arXiv 2306.11975).
+
+The product is the C-ABI library ``libozimmu.so`` (include/ozimmu.h) built from
+``csrc/`` for sm_100a; this package is its thin Python binding plus the
+multi-GPU driver.  No CPU fallback exists.
+"""
+from .ozimmu import (EXPORTS, Handle, OzimmuError, b_slices_bytes, lib, version,  # noqa: F401
+                     workspace_bytes)
+
+__all__ = ["Handle", "OzimmuError", "lib", "version", "workspace_bytes", "b_slices_bytes",
+           "EXPORTS"]

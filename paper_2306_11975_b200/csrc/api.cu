@@ -1,0 +1,487 @@
+// api.cu -- host runtime behind include/ozimmu.h: handle, argument validation, plan,
+// workspace, and the launch sequence  slice(A) -> slice(B) -> fused tcgen05 GEMM+epilogue.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "../../include/ozimmu.h"
+#include "internal.h"
+
+using namespace ozimmu;
+
+struct ozimmu_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    void *user_ws = nullptr;
+    size_t user_ws_bytes = 0;
+    void *own_ws = nullptr;
+    size_t own_ws_bytes = 0;
+    ozimmu_report_t report{};
+};
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Layout {  // workspace carve-up for one dgemm call
+    size_t a_planes, a_exp, b_buf, keys, scratch, total;
+};
+
+// B-slice buffer: planes [s][n][k_pad] (reversed slice order) | int32 exponents [n]
+size_t b_buf_planes_bytes(int64_t n, int64_t k_pad, int s) {
+    return align_up((size_t)s * (size_t)n * (size_t)k_pad);
+}
+size_t b_buf_bytes(int64_t n, int64_t k_pad, int s) {
+    return b_buf_planes_bytes(n, k_pad, s) + align_up(sizeof(int32_t) * (size_t)n);
+}
+
+Layout layout(int64_t m, int64_t n, int64_t k_pad, int s, size_t scratch) {
+    Layout L;
+    size_t off = 0;
+    L.a_planes = off;
+    off += align_up((size_t)s * m * k_pad);
+    L.a_exp = off;
+    off += align_up(sizeof(int32_t) * (size_t)m);
+    L.b_buf = off;
+    off += b_buf_bytes(n, k_pad, s);
+    L.keys = off;
+    off += align_up(sizeof(int32_t) * (size_t)(m > n ? m : n));
+    L.scratch = off;
+    off += align_up(scratch);
+    L.total = off;
+    return L;
+}
+
+bool valid_op(ozimmu_op_t op) { return op == OZIMMU_OP_N || op == OZIMMU_OP_T || op == OZIMMU_OP_C; }
+
+ozimmu_status_t get_ws(ozimmu_handle_t h, size_t need, void **ws) {
+    if (h->user_ws) {
+        if (need > h->user_ws_bytes) return OZIMMU_ERR_WORKSPACE;
+        *ws = h->user_ws;
+        return OZIMMU_SUCCESS;
+    }
+    if (need > h->own_ws_bytes) {
+        if (h->own_ws) {
+            cudaStreamSynchronize(h->stream);  // the old buffer may be in use by queued work
+            cudaFree(h->own_ws);
+            h->own_ws = nullptr;
+            h->own_ws_bytes = 0;
+        }
+        size_t sz = need + need / 8;
+        if (cudaMalloc(&h->own_ws, sz) != cudaSuccess) {
+            cudaGetLastError();
+            return OZIMMU_ERR_WORKSPACE;
+        }
+        h->own_ws_bytes = sz;
+    }
+    *ws = h->own_ws;
+    return OZIMMU_SUCCESS;
+}
+
+__global__ void k_scale_c(double *C, int64_t ldc, int64_t m, int64_t n, double beta) {
+    const int64_t total = m * n;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % m, j = t / m;
+        double *c = C + i + j * ldc;
+        *c = beta == 0.0 ? 0.0 : __dmul_rn(beta, *c);
+    }
+}
+
+ozimmu_status_t cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return OZIMMU_SUCCESS;
+    cudaGetLastError();
+    return OZIMMU_ERR_CUDA;
+}
+
+// Common validation for the A side and the sizes.
+ozimmu_status_t check_common(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t n,
+                             int64_t k, const double *alpha, const double *A, int64_t lda,
+                             const double *beta, double *C, int64_t ldc, int s) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!valid_op(transA)) return OZIMMU_ERR_INVALID_VALUE;
+    if (m < 0 || n < 0 || k < 0) return OZIMMU_ERR_INVALID_VALUE;
+    if (!alpha || !beta) return OZIMMU_ERR_INVALID_VALUE;
+    const int64_t arows = transA == OZIMMU_OP_N ? m : k;
+    if (lda < (arows > 1 ? arows : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (ldc < (m > 1 ? m : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (m > 0 && n > 0 && !C) return OZIMMU_ERR_INVALID_VALUE;
+    if (m > 0 && k > 0 && *alpha != 0.0 && !A) return OZIMMU_ERR_INVALID_VALUE;
+    if (s == 0) return OZIMMU_ERR_UNSUPPORTED;  // INT8-AUTO not implemented
+    if (s < 0 || s > OZIMMU_MAX_SLICES) return OZIMMU_ERR_INVALID_VALUE;
+    if (k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    return OZIMMU_SUCCESS;
+}
+
+void fill_report(ozimmu_handle_t h, int s, int w, int64_t m, int64_t n, int64_t k,
+                 const GemmPlan *gp, int launches, int64_t slice_bytes) {
+    ozimmu_report_t &r = h->report;
+    r.num_slices = s;
+    r.slice_width = w;
+    r.gemm_pairs = (int64_t)s * (s + 1) / 2;
+    r.int8_macs = r.gemm_pairs * m * n * k;
+    r.slice_bytes = slice_bytes;
+    r.tile_n = gp ? gp->tile_n : 0;
+    r.k_block = gp ? gp->k_block : 0;
+    r.stages = gp ? gp->stages : 0;
+    r.k_chunks = gp ? gp->k_chunks : 0;
+    r.launches = launches;
+}
+
+// C = beta C (alpha == 0 or k == 0 quick return; A and B are not read).
+ozimmu_status_t scale_only(ozimmu_handle_t h, int64_t m, int64_t n, double beta, double *C,
+                           int64_t ldc) {
+    int launches = 0;
+    if (beta != 1.0) {
+        int64_t blocks = ceil_div(m * n, 256);
+        if (blocks > 8 * (int64_t)h->num_sms) blocks = 8 * (int64_t)h->num_sms;
+        k_scale_c<<<(unsigned)blocks, 256, 0, h->stream>>>(C, ldc, m, n, beta);
+        ++launches;
+        if (cudaGetLastError() != cudaSuccess) return OZIMMU_ERR_CUDA;
+    }
+    fill_report(h, 0, 0, m, n, 0, nullptr, launches, 0);
+    return OZIMMU_SUCCESS;
+}
+
+// Slice op(A): rows of op(A) are contiguous along k iff transA != N.
+cudaError_t slice_a(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t k, int64_t k_pad,
+                    const double *A, int64_t lda, int s, int w, int8_t *planes, int32_t *E,
+                    int32_t *keys, int *launches) {
+    const bool contig = transA != OZIMMU_OP_N;
+    return launch_split(A, lda, contig, m, k, k_pad, s, w, /*reverse=*/false, planes,
+                        (int64_t)m * k_pad, E, keys, h->num_sms, h->stream, launches);
+}
+
+// Slice op(B) into a B-slice buffer: columns of op(B) are contiguous along k iff transB == N.
+cudaError_t slice_b(ozimmu_handle_t h, ozimmu_op_t transB, int64_t k, int64_t n, int64_t k_pad,
+                    const double *B, int64_t ldb, int s, int w, uint8_t *bbuf, int32_t *keys,
+                    int *launches) {
+    const bool contig = transB == OZIMMU_OP_N;
+    int8_t *planes = reinterpret_cast<int8_t *>(bbuf);
+    int32_t *E = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
+    return launch_split(B, ldb, contig, n, k, k_pad, s, w, /*reverse=*/true, planes,
+                        (int64_t)n * k_pad, E, keys, h->num_sms, h->stream, launches);
+}
+
+ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t n, int64_t k,
+                          double alpha, const double *A, int64_t lda, const uint8_t *bbuf_ext,
+                          ozimmu_op_t transB, const double *B, int64_t ldb, double beta,
+                          double *C, int64_t ldc, int s) {
+    const int w = slice_width(k);
+    const int64_t k_pad = round_up(k, 16);
+    GemmPlan gp;
+    if (!plan_gemm(s, w, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
+    const Layout L = layout(m, bbuf_ext ? 0 : n, k_pad, s, chunk_scratch_bytes(gp, s));
+    void *ws = nullptr;
+    ozimmu_status_t st = get_ws(h, L.total, &ws);
+    if (st) return st;
+    uint8_t *base = static_cast<uint8_t *>(ws);
+    int8_t *a_planes = reinterpret_cast<int8_t *>(base + L.a_planes);
+    int32_t *EA = reinterpret_cast<int32_t *>(base + L.a_exp);
+    int32_t *keys = reinterpret_cast<int32_t *>(base + L.keys);
+    const uint8_t *bbuf = bbuf_ext;
+    int launches = 0;
+    int64_t slice_bytes = (int64_t)s * m * k_pad + 4 * m;
+    if (!bbuf_ext) {
+        uint8_t *b = base + L.b_buf;
+        cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, b, keys, &launches);
+        if (e != cudaSuccess) return cuda_status(e);
+        bbuf = b;
+        slice_bytes += (int64_t)s * n * k_pad + 4 * n;
+    }
+    cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    GemmArgs ga{};
+    ga.a_planes = a_planes;
+    ga.b_planes = reinterpret_cast<const int8_t *>(bbuf);
+    ga.EA = EA;
+    ga.EB = reinterpret_cast<const int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
+    ga.m = m;
+    ga.n = n;
+    ga.k_pad = k_pad;
+    ga.s = s;
+    ga.w = w;
+    ga.alpha = alpha;
+    ga.beta = beta;
+    ga.C = C;
+    ga.ldc = ldc;
+    ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
+    e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    fill_report(h, s, w, m, n, k, &gp, launches, slice_bytes);
+    return OZIMMU_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ozimmu_version(void) { return 100; }
+
+const char *ozimmu_status_string(ozimmu_status_t s) {
+    switch (s) {
+    case OZIMMU_SUCCESS: return "OZIMMU_SUCCESS";
+    case OZIMMU_ERR_INVALID_VALUE: return "OZIMMU_ERR_INVALID_VALUE";
+    case OZIMMU_ERR_UNSUPPORTED: return "OZIMMU_ERR_UNSUPPORTED";
+    case OZIMMU_ERR_WORKSPACE: return "OZIMMU_ERR_WORKSPACE";
+    case OZIMMU_ERR_CUDA: return "OZIMMU_ERR_CUDA";
+    case OZIMMU_ERR_NOT_INITIALIZED: return "OZIMMU_ERR_NOT_INITIALIZED";
+    }
+    return "OZIMMU_UNKNOWN_STATUS";
+}
+
+ozimmu_status_t ozimmu_create(ozimmu_handle_t *h, int device) {
+    if (!h) return OZIMMU_ERR_INVALID_VALUE;
+    *h = nullptr;
+    int major = 0, minor = 0, sms = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        cudaGetLastError();
+        return OZIMMU_ERR_CUDA;
+    }
+    if (major != 10 || minor != 0) return OZIMMU_ERR_CUDA;  // sm_100a binary only
+    ozimmu_ctx *c = new ozimmu_ctx();
+    c->device = device;
+    c->num_sms = sms;
+    *h = c;
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
+    if (!h) return OZIMMU_SUCCESS;
+    if (h->own_ws) {
+        cudaStreamSynchronize(h->stream);
+        cudaFree(h->own_ws);
+    }
+    delete h;
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_set_stream(ozimmu_handle_t h, void *stream) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    h->stream = static_cast<cudaStream_t>(stream);
+    return OZIMMU_SUCCESS;
+}
+
+size_t ozimmu_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m, int64_t n,
+                              int64_t k, int num_slices) {
+    if (!valid_op(transA) || !valid_op(transB) || m < 0 || n < 0 || k < 1 || num_slices < 1 ||
+        num_slices > OZIMMU_MAX_SLICES || k > OZIMMU_MAX_K)
+        return 0;
+    const int w = slice_width(k);
+    const int64_t k_pad = round_up(k, 16);
+    GemmPlan gp;
+    if (!plan_gemm(num_slices, w, m > 0 ? m : 1, n > 0 ? n : 1, k_pad, 148, &gp)) return 0;
+    gp.grid = gp.grid < 148 ? 148 : gp.grid;  // upper bound over devices up to 148 SMs
+    return layout(m, n, k_pad, num_slices, chunk_scratch_bytes(gp, num_slices)).total;
+}
+
+ozimmu_status_t ozimmu_set_workspace(ozimmu_handle_t h, void *dptr, size_t bytes) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (dptr && (reinterpret_cast<uintptr_t>(dptr) % kAlign) != 0) return OZIMMU_ERR_INVALID_VALUE;
+    h->user_ws = dptr;
+    h->user_ws_bytes = dptr ? bytes : 0;
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_get_report(ozimmu_handle_t h, ozimmu_report_t *out) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!out) return OZIMMU_ERR_INVALID_VALUE;
+    *out = h->report;
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_dgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
+                             int64_t n, int64_t k, const double *alpha, const double *A,
+                             int64_t lda, const double *B, int64_t ldb, const double *beta,
+                             double *C, int64_t ldc, int num_slices) {
+    ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc, num_slices);
+    if (st) return st;
+    if (!valid_op(transB)) return OZIMMU_ERR_INVALID_VALUE;
+    const int64_t brows = transB == OZIMMU_OP_N ? k : n;
+    if (ldb < (brows > 1 ? brows : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (n > 0 && k > 0 && m > 0 && *alpha != 0.0 && !B) return OZIMMU_ERR_INVALID_VALUE;
+    if (m == 0 || n == 0) {
+        fill_report(h, 0, 0, m, n, k, nullptr, 0, 0);
+        return OZIMMU_SUCCESS;
+    }
+    if (*alpha == 0.0 || k == 0) return scale_only(h, m, n, *beta, C, ldc);
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    return gemm_core(h, transA, m, n, k, *alpha, A, lda, nullptr, transB, B, ldb, *beta, C, ldc,
+                     num_slices);
+}
+
+size_t ozimmu_b_slices_bytes(int64_t n, int64_t k, int num_slices) {
+    if (n < 0 || k < 1 || num_slices < 1 || num_slices > OZIMMU_MAX_SLICES) return 0;
+    return b_buf_bytes(n, round_up(k, 16), num_slices);
+}
+
+ozimmu_status_t ozimmu_slice_b(ozimmu_handle_t h, ozimmu_op_t transB, int64_t k, int64_t n,
+                               const double *B, int64_t ldb, int num_slices, void *b_slices) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!valid_op(transB) || k < 1 || n < 0) return OZIMMU_ERR_INVALID_VALUE;
+    if (num_slices == 0) return OZIMMU_ERR_UNSUPPORTED;
+    if (num_slices < 0 || num_slices > OZIMMU_MAX_SLICES) return OZIMMU_ERR_INVALID_VALUE;
+    if (k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    const int64_t brows = transB == OZIMMU_OP_N ? k : n;
+    if (ldb < (brows > 1 ? brows : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (n == 0) return OZIMMU_SUCCESS;
+    if (!B || !b_slices) return OZIMMU_ERR_INVALID_VALUE;
+    if (reinterpret_cast<uintptr_t>(b_slices) % kAlign) return OZIMMU_ERR_INVALID_VALUE;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    const int64_t k_pad = round_up(k, 16);
+    void *ws = nullptr;
+    ozimmu_status_t st = get_ws(h, align_up(sizeof(int32_t) * (size_t)n), &ws);
+    if (st) return st;
+    int launches = 0;
+    cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, num_slices, slice_width(k),
+                            static_cast<uint8_t *>(b_slices), static_cast<int32_t *>(ws), &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    fill_report(h, num_slices, slice_width(k), 0, n, k, nullptr, launches,
+                (int64_t)num_slices * n * k_pad + 4 * n);
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_dgemm_presliced_b(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m,
+                                         int64_t n, int64_t k, const double *alpha,
+                                         const double *A, int64_t lda, const void *b_slices,
+                                         const double *beta, double *C, int64_t ldc,
+                                         int num_slices) {
+    ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc, num_slices);
+    if (st) return st;
+    if (m == 0 || n == 0) {
+        fill_report(h, 0, 0, m, n, k, nullptr, 0, 0);
+        return OZIMMU_SUCCESS;
+    }
+    if (*alpha == 0.0 || k == 0) return scale_only(h, m, n, *beta, C, ldc);
+    if (!b_slices || reinterpret_cast<uintptr_t>(b_slices) % kAlign) return OZIMMU_ERR_INVALID_VALUE;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    return gemm_core(h, transA, m, n, k, *alpha, A, lda, static_cast<const uint8_t *>(b_slices),
+                     OZIMMU_OP_N, nullptr, 0, *beta, C, ldc, num_slices);
+}
+
+ozimmu_status_t ozimmu_debug_split(ozimmu_handle_t h, ozimmu_op_t op, int is_rows, int64_t rows,
+                                   int64_t kdim, const double *M, int64_t ld, int num_slices,
+                                   int8_t *planes_out, int32_t *exps_out) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!valid_op(op) || rows < 0 || kdim < 1 || num_slices < 1 ||
+        num_slices > OZIMMU_MAX_SLICES)
+        return OZIMMU_ERR_INVALID_VALUE;
+    if (kdim > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    if (rows == 0) return OZIMMU_SUCCESS;
+    if (!M || !planes_out || !exps_out) return OZIMMU_ERR_INVALID_VALUE;
+    // vector r element l: A operand (is_rows): op(M)(r,l); B operand: op(M)(l,r)
+    const bool contig = is_rows ? (op != OZIMMU_OP_N) : (op == OZIMMU_OP_N);
+    const int64_t min_ld = contig ? kdim : rows;
+    if (ld < (min_ld > 1 ? min_ld : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    const int w = slice_width(kdim);
+    const int64_t k_pad = round_up(kdim, 16);
+    const size_t pbytes = align_up((size_t)num_slices * rows * k_pad);
+    void *ws = nullptr;
+    ozimmu_status_t st = get_ws(h, pbytes + align_up(4 * (size_t)rows), &ws);
+    if (st) return st;
+    int8_t *planes = static_cast<int8_t *>(ws);
+    int32_t *keys = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(ws) + pbytes);
+    int launches = 0;
+    cudaError_t e = launch_split(M, ld, contig, rows, kdim, k_pad, num_slices, w, false, planes,
+                                 rows * k_pad, exps_out, keys, h->num_sms, h->stream, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    // repack [s][rows][k_pad] -> [s][rows][kdim]
+    e = cudaMemcpy2DAsync(planes_out, (size_t)kdim, planes, (size_t)k_pad, (size_t)kdim,
+                          (size_t)num_slices * rows, cudaMemcpyDeviceToDevice, h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    fill_report(h, num_slices, w, rows, 0, kdim, nullptr, launches, (int64_t)pbytes);
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_debug_level_sums(ozimmu_handle_t h, ozimmu_op_t transA,
+                                        ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                        const double *A, int64_t lda, const double *B,
+                                        int64_t ldb, int num_slices, int64_t *Lg_out) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!valid_op(transA) || !valid_op(transB) || m < 1 || n < 1 || k < 1 || !A || !B || !Lg_out)
+        return OZIMMU_ERR_INVALID_VALUE;
+    if (lda < (transA == OZIMMU_OP_N ? m : k) || ldb < (transB == OZIMMU_OP_N ? k : n))
+        return OZIMMU_ERR_INVALID_VALUE;
+    if (num_slices < 1 || num_slices > OZIMMU_MAX_SLICES) return OZIMMU_ERR_INVALID_VALUE;
+    if (k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    ozimmu_status_t st;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    const int s = num_slices;
+    const int w = slice_width(k);
+    const int64_t k_pad = round_up(k, 16);
+    GemmPlan gp;
+    if (!plan_gemm(s, w, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
+    const Layout L = layout(m, n, k_pad, s, chunk_scratch_bytes(gp, s));
+    void *ws = nullptr;
+    if ((st = get_ws(h, L.total, &ws))) return st;
+    uint8_t *base = static_cast<uint8_t *>(ws);
+    int launches = 0;
+    int32_t *keys = reinterpret_cast<int32_t *>(base + L.keys);
+    cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, base + L.b_buf, keys, &launches);
+    if (e == cudaSuccess)
+        e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, reinterpret_cast<int8_t *>(base + L.a_planes),
+                    reinterpret_cast<int32_t *>(base + L.a_exp), keys, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    GemmArgs ga{};
+    ga.a_planes = reinterpret_cast<const int8_t *>(base + L.a_planes);
+    ga.b_planes = reinterpret_cast<const int8_t *>(base + L.b_buf);
+    ga.m = m;
+    ga.n = n;
+    ga.k_pad = k_pad;
+    ga.s = s;
+    ga.w = w;
+    ga.out = Lg_out;
+    ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
+    e = launch_gemm(ga, gp, EPI_LEVELS_I64, h->stream, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    fill_report(h, s, w, m, n, k, &gp, launches, 0);
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_debug_pair(ozimmu_handle_t h, const int8_t *Ai, const int8_t *Bj, int64_t m,
+                                  int64_t n, int64_t k, int32_t *P_out) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (m < 1 || n < 1 || k < 1 || !Ai || !Bj || !P_out) return OZIMMU_ERR_INVALID_VALUE;
+    if (k > 133144) return OZIMMU_ERR_UNSUPPORTED;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    const int64_t k_pad = round_up(k, 16);
+    GemmPlan gp;
+    if (!plan_gemm(1, 7, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
+    gp.chunk_blocks = gp.num_k_blocks;  // caller guarantees the INT32 budget
+    gp.k_chunks = 1;
+    const size_t abytes = align_up((size_t)m * k_pad), bbytes = align_up((size_t)n * k_pad);
+    void *ws = nullptr;
+    ozimmu_status_t st = get_ws(h, abytes + bbytes, &ws);
+    if (st) return st;
+    int8_t *a = static_cast<int8_t *>(ws);
+    int8_t *b = a + abytes;
+    cudaError_t e = cudaMemsetAsync(ws, 0, abytes + bbytes, h->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(a, k_pad, Ai, k, k, m, cudaMemcpyDeviceToDevice, h->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(b, k_pad, Bj, k, k, n, cudaMemcpyDeviceToDevice, h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    GemmArgs ga{};
+    ga.a_planes = a;
+    ga.b_planes = b;
+    ga.m = m;
+    ga.n = n;
+    ga.k_pad = k_pad;
+    ga.s = 1;
+    ga.w = 7;
+    ga.out = P_out;
+    int launches = 0;
+    e = launch_gemm(ga, gp, EPI_PAIR_I32, h->stream, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    fill_report(h, 1, 7, m, n, k, &gp, launches, 0);
+    return OZIMMU_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// internal.h -- host-side plan and kernel launchers shared by api.cu, split.cu, igemm.cu.
+// Not part of the public ABI (see include/ozimmu.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ozimmu {
+
+constexpr int32_t kExpNonFinite = 0x7fffffff;   // == OZIMMU_EXP_NONFINITE
+constexpr int32_t kKeyEmpty = (int32_t)0x80808080;  // memset(0x80) pattern: "no nonzero seen"
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+inline int64_t ceil_div(int64_t x, int64_t a) { return (x + a - 1) / a; }
+
+// A1 (Eq. alpha P:224-227 with l_acc = 31, BPS P:457-460 with l_in = 7):
+// w = min(7, floor((31 - ceil(log2 k)) / 2)) -- the integer form of floor((31 - log2 k)/2).
+inline int slice_width(int64_t k) {
+    int c = 0;
+    while (((int64_t)1 << c) < k) ++c;  // c = ceil(log2 k)
+    int a = (31 - c) / 2;
+    return a < 7 ? a : 7;
+}
+
+// ---- slicing (A2 + A3) -------------------------------------------------------------
+// Vectors r = 0..rows-1 of length kdim; element l of vector r is
+//   contiguous ? M[l + r*ld] : M[r + l*ld].
+// Output planes: slice p (1..s) of vector r at planes + pidx*plane_stride + r*k_pad + l,
+// pidx = reverse ? s - p : p - 1;  elements l in [kdim, k_pad) are written as 0.
+// E[r]: frexp exponent of the vector's max |x| (0 for an all-zero vector,
+// kExpNonFinite if any element is NaN/Inf -- its digits are then all 0).
+// key_scratch: int32[rows] device scratch (strided case only).
+cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
+                         int64_t k_pad, int s, int w, bool reverse, int8_t *planes,
+                         int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
+                         cudaStream_t st, int *launches);
+
+// ---- fused GEMM (A4 + A5) ----------------------------------------------------------------
+enum EpiMode : int { EPI_DGEMM = 0, EPI_LEVELS_I64 = 1, EPI_PAIR_I32 = 2 };
+
+struct GemmArgs {
+    const int8_t *a_planes;  // [s][m][k_pad], natural slice order
+    const int8_t *b_planes;  // [s][n][k_pad], REVERSED slice order (index s - q)
+    const int32_t *EA, *EB;  // exponents (EPI_DGEMM only)
+    int64_t m, n, k_pad;
+    int s, w;
+    double alpha, beta;
+    double *C;               // EPI_DGEMM: column-major, ldc
+    int64_t ldc;
+    void *out;               // EPI_LEVELS_I64: int64 [s][n][m];  EPI_PAIR_I32: int32 [n][m]
+    int64_t *chunk_scratch;  // per-CTA partial level sums when k_chunks > 1
+};
+
+struct GemmPlan {
+    int tile_n;       // N_c
+    int k_block;      // K bytes per stage (= swizzle width)
+    int stages;
+    int64_t num_k_blocks;
+    int64_t chunk_blocks;  // k-blocks per INT32-safe chunk
+    int k_chunks;
+    int grid;
+    size_t smem_bytes;
+    int tmem_cols;
+};
+
+// Choose tile/pipeline parameters for (s, w, k_pad); returns false if unsupported.
+bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, GemmPlan *p);
+size_t chunk_scratch_bytes(const GemmPlan &p, int s);
+cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st,
+                        int *launches);
+
+}  // namespace ozimmu

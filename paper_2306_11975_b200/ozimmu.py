@@ -1,0 +1,203 @@
+"""Thin ctypes binding over libozimmu.so (include/ozimmu.h).
+
+Argument marshalling only: every step of the method runs in the library's
+sm_100a kernels.  PyTorch is used for device memory and streams.  There is no
+CPU fallback: if the CUDA library cannot be loaded, or a call fails, an
+exception is raised.
+
+The raw entry points keep the C names and BLAS argument order (column-major,
+device pointers as ints, alpha/beta as Python floats).  ``matmul`` is the
+row-major torch convenience (C = A @ B via C^T = B^T A^T, bitwise identical).
+"""
+import ctypes as ct
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libozimmu.so")
+
+OP = {"N": 0, "T": 1, "C": 2, 0: 0, 1: 1, 2: 2}
+STATUS = {0: "OZIMMU_SUCCESS", 1: "OZIMMU_ERR_INVALID_VALUE", 2: "OZIMMU_ERR_UNSUPPORTED",
+          3: "OZIMMU_ERR_WORKSPACE", 4: "OZIMMU_ERR_CUDA", 5: "OZIMMU_ERR_NOT_INITIALIZED"}
+EXP_NONFINITE = 0x7FFFFFFF
+
+# Every symbol include/ozimmu.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "ozimmu_create", "ozimmu_destroy", "ozimmu_set_stream", "ozimmu_workspace_bytes",
+    "ozimmu_set_workspace", "ozimmu_get_report", "ozimmu_version", "ozimmu_status_string",
+    "ozimmu_dgemm", "ozimmu_b_slices_bytes", "ozimmu_slice_b", "ozimmu_dgemm_presliced_b",
+    "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
+]
+
+
+class OzimmuError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} failed: {STATUS.get(code, code)}")
+        self.code = code
+
+
+class Report(ct.Structure):
+    _fields_ = [("num_slices", ct.c_int), ("slice_width", ct.c_int),
+                ("gemm_pairs", ct.c_int64), ("int8_macs", ct.c_int64),
+                ("slice_bytes", ct.c_int64), ("tile_n", ct.c_int), ("k_block", ct.c_int),
+                ("stages", ct.c_int), ("k_chunks", ct.c_int), ("launches", ct.c_int)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libozimmu.so (built in-tree by build.py / __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; "
+                           "g.build()'` (no CPU fallback exists)")
+    L = ct.CDLL(LIB_PATH)
+    i64, i32, vp, dp, sz = ct.c_int64, ct.c_int, ct.c_void_p, ct.POINTER(ct.c_double), ct.c_size_t
+    H = ct.c_void_p
+    sig = {
+        "ozimmu_create": ([ct.POINTER(H), i32], i32),
+        "ozimmu_destroy": ([H], i32),
+        "ozimmu_set_stream": ([H, vp], i32),
+        "ozimmu_workspace_bytes": ([i32, i32, i64, i64, i64, i32], sz),
+        "ozimmu_set_workspace": ([H, vp, sz], i32),
+        "ozimmu_get_report": ([H, ct.POINTER(Report)], i32),
+        "ozimmu_version": ([], i32),
+        "ozimmu_status_string": ([i32], ct.c_char_p),
+        "ozimmu_dgemm": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32], i32),
+        "ozimmu_b_slices_bytes": ([i64, i64, i32], sz),
+        "ozimmu_slice_b": ([H, i32, i64, i64, vp, i64, i32, vp], i32),
+        "ozimmu_dgemm_presliced_b": ([H, i32, i64, i64, i64, dp, vp, i64, vp, dp, vp, i64, i32], i32),
+        "ozimmu_debug_split": ([H, i32, i32, i64, i64, vp, i64, i32, vp, vp], i32),
+        "ozimmu_debug_level_sums": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, i32, vp], i32),
+        "ozimmu_debug_pair": ([H, vp, vp, i64, i64, i64, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(fn, rc):
+    if rc != 0:
+        raise OzimmuError(fn, rc)
+
+
+def _d(x):
+    return ct.byref(ct.c_double(float(x)))
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor (or an int)."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def workspace_bytes(transA, transB, m, n, k, num_slices):
+    return int(lib().ozimmu_workspace_bytes(OP[transA], OP[transB], m, n, k, num_slices))
+
+
+def b_slices_bytes(n, k, num_slices):
+    return int(lib().ozimmu_b_slices_bytes(n, k, num_slices))
+
+
+def version():
+    return int(lib().ozimmu_version())
+
+
+class Handle:
+    """Owns an ozimmu handle bound to one CUDA device."""
+
+    def __init__(self, device=0):
+        self._h = ct.c_void_p()
+        _check("ozimmu_create", lib().ozimmu_create(ct.byref(self._h), int(device)))
+        self.device = device
+        self._ws = None
+
+    def close(self):
+        if self._h:
+            lib().ozimmu_destroy(self._h)
+            self._h = ct.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- plumbing ---------------------------------------------------------------
+    def set_stream(self, stream):
+        """stream: torch.cuda.Stream, raw cudaStream_t int, or None (legacy default)."""
+        raw = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+        _check("ozimmu_set_stream", lib().ozimmu_set_stream(self._h, raw))
+
+    def set_workspace(self, tensor_or_ptr, nbytes=None):
+        if tensor_or_ptr is None:
+            self._ws = None
+            _check("ozimmu_set_workspace", lib().ozimmu_set_workspace(self._h, None, 0))
+            return
+        if nbytes is None:
+            nbytes = tensor_or_ptr.numel() * tensor_or_ptr.element_size()
+        self._ws = tensor_or_ptr  # keep alive
+        _check("ozimmu_set_workspace",
+               lib().ozimmu_set_workspace(self._h, _ptr(tensor_or_ptr), int(nbytes)))
+
+    def report(self):
+        r = Report()
+        _check("ozimmu_get_report", lib().ozimmu_get_report(self._h, ct.byref(r)))
+        return r.as_dict()
+
+    # -- the C ABI, same names and argument order ---------------------------------
+    def dgemm(self, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_slices):
+        _check("ozimmu_dgemm", lib().ozimmu_dgemm(
+            self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _ptr(A), lda, _ptr(B), ldb,
+            _d(beta), _ptr(C), ldc, int(num_slices)))
+
+    def slice_b(self, transB, k, n, B, ldb, num_slices, b_slices):
+        _check("ozimmu_slice_b", lib().ozimmu_slice_b(
+            self._h, OP[transB], k, n, _ptr(B), ldb, int(num_slices), _ptr(b_slices)))
+
+    def dgemm_presliced_b(self, transA, m, n, k, alpha, A, lda, b_slices, beta, C, ldc,
+                          num_slices):
+        _check("ozimmu_dgemm_presliced_b", lib().ozimmu_dgemm_presliced_b(
+            self._h, OP[transA], m, n, k, _d(alpha), _ptr(A), lda, _ptr(b_slices), _d(beta),
+            _ptr(C), ldc, int(num_slices)))
+
+    def debug_split(self, op, is_rows, rows, kdim, M, ld, num_slices, planes_out, exps_out):
+        _check("ozimmu_debug_split", lib().ozimmu_debug_split(
+            self._h, OP[op], int(is_rows), rows, kdim, _ptr(M), ld, int(num_slices),
+            _ptr(planes_out), _ptr(exps_out)))
+
+    def debug_level_sums(self, transA, transB, m, n, k, A, lda, B, ldb, num_slices, Lg_out):
+        _check("ozimmu_debug_level_sums", lib().ozimmu_debug_level_sums(
+            self._h, OP[transA], OP[transB], m, n, k, _ptr(A), lda, _ptr(B), ldb,
+            int(num_slices), _ptr(Lg_out)))
+
+    def debug_pair(self, Ai, Bj, m, n, k, P_out):
+        _check("ozimmu_debug_pair", lib().ozimmu_debug_pair(
+            self._h, _ptr(Ai), _ptr(Bj), m, n, k, _ptr(P_out)))
+
+    # -- torch convenience --------------------------------------------------------
+    def matmul(self, A, B, num_slices, out=None):
+        """Row-major torch float64 CUDA tensors: returns A @ B (m x n) computed by the
+        Ozaki scheme.  Uses C^T = B^T A^T on the column-major ABI."""
+        import torch
+        assert A.is_cuda and B.is_cuda and A.dtype == torch.float64 and B.dtype == torch.float64
+        A = A.contiguous()
+        B = B.contiguous()
+        m, k = A.shape
+        k2, n = B.shape
+        assert k == k2
+        if out is None:
+            out = torch.empty((m, n), dtype=torch.float64, device=A.device)
+        self.dgemm("N", "N", n, m, k, 1.0, B, n, A, k, 0.0, out, n, num_slices)
+        return out
