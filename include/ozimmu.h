@@ -112,6 +112,19 @@ OZIMMU_API size_t ozimmu_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB,
 OZIMMU_API ozimmu_status_t ozimmu_set_workspace(ozimmu_handle_t h, void *dptr, size_t bytes);
 /* Copy the report of the last computing call. */
 OZIMMU_API ozimmu_status_t ozimmu_get_report(ozimmu_handle_t h, ozimmu_report_t *out);
+/* Per-phase device time of one computing call, from CUDA events the library records on
+ * the handle's stream around each of its kernels (the paper's time breakdown). */
+typedef struct {
+    float slice_b_ms; /* A2+A3 on op(B) (0 for presliced calls) */
+    float slice_a_ms; /* A2+A3 on op(A) */
+    float gemm_ms;    /* A4+A5: the fused tcgen05 GEMM + epilogue kernel */
+} ozimmu_timing_t;
+/* Start recording phase events for the next `max_calls` computing calls (0 disables and
+ * frees the events).  Recording adds event records only -- no synchronisation. */
+OZIMMU_API ozimmu_status_t ozimmu_timing_enable(ozimmu_handle_t h, int max_calls);
+/* Wait for the recorded events, copy up to max_out per-call timings to out, return the
+ * number of recorded calls (< 0 on error), and restart recording from an empty ring. */
+OZIMMU_API int ozimmu_timing_read(ozimmu_handle_t h, ozimmu_timing_t *out, int max_out);
 /* Library version (major*10000 + minor*100 + patch). */
 OZIMMU_API int ozimmu_version(void);
 /* Human-readable status name (static string). */

@@ -19,6 +19,10 @@ struct ozimmu_ctx {
     void *own_ws = nullptr;
     size_t own_ws_bytes = 0;
     ozimmu_report_t report{};
+    // phase timing ring (ozimmu_timing_enable / _read)
+    cudaEvent_t *events = nullptr;
+    int timing_cap = 0;
+    int timing_count = 0;
 };
 
 namespace {
@@ -28,7 +32,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {  // workspace carve-up for one dgemm call
-    size_t a_planes, a_exp, b_buf, keys, scratch, total;
+    size_t a_planes, a_exp, b_buf, keys, sync, scratch, total;
 };
 
 // B-slice buffer: planes [s][n][k_pad] (reversed slice order) | int32 exponents [n]
@@ -50,6 +54,8 @@ Layout layout(int64_t m, int64_t n, int64_t k_pad, int s, size_t scratch) {
     off += b_buf_bytes(n, k_pad, s);
     L.keys = off;
     off += align_up(sizeof(int32_t) * (size_t)(m > n ? m : n));
+    L.sync = off;
+    off += kAlign;
     L.scratch = off;
     off += align_up(scratch);
     L.total = off;
@@ -90,6 +96,15 @@ __global__ void k_scale_c(double *C, int64_t ldc, int64_t m, int64_t n, double b
         double *c = C + i + j * ldc;
         *c = beta == 0.0 ? 0.0 : __dmul_rn(beta, *c);
     }
+}
+
+// Record phase event `ph` (0..3) of the current call if timing is on.
+inline void mark(ozimmu_handle_t h, int ph) {
+    if (h->timing_cap && h->timing_count < h->timing_cap)
+        cudaEventRecord(h->events[4 * h->timing_count + ph], h->stream);
+}
+inline void mark_done(ozimmu_handle_t h) {
+    if (h->timing_cap && h->timing_count < h->timing_cap) ++h->timing_count;
 }
 
 ozimmu_status_t cuda_status(cudaError_t e) {
@@ -186,6 +201,7 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     const uint8_t *bbuf = bbuf_ext;
     int launches = 0;
     int64_t slice_bytes = (int64_t)s * m * k_pad + 4 * m;
+    mark(h, 0);
     if (!bbuf_ext) {
         uint8_t *b = base + L.b_buf;
         cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, b, keys, &launches);
@@ -193,8 +209,10 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
         bbuf = b;
         slice_bytes += (int64_t)s * n * k_pad + 4 * n;
     }
+    mark(h, 1);
     cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches);
     if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 2);
     GemmArgs ga{};
     ga.a_planes = a_planes;
     ga.b_planes = reinterpret_cast<const int8_t *>(bbuf);
@@ -210,8 +228,13 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     ga.C = C;
     ga.ldc = ldc;
     ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
+    // soft per-wave grid barrier (L2 reuse); OZIMMU_NO_WAVE_SYNC=1 disables (experiments)
+    static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
+    ga.wave_counter = no_sync ? nullptr : reinterpret_cast<unsigned int *>(base + L.sync);
     e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, &launches);
     if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 3);
+    mark_done(h);
     fill_report(h, s, w, m, n, k, &gp, launches, slice_bytes);
     return OZIMMU_SUCCESS;
 }
@@ -252,8 +275,61 @@ ozimmu_status_t ozimmu_create(ozimmu_handle_t *h, int device) {
     return OZIMMU_SUCCESS;
 }
 
+ozimmu_status_t ozimmu_timing_enable(ozimmu_handle_t h, int max_calls) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (max_calls < 0 || max_calls > 1 << 16) return OZIMMU_ERR_INVALID_VALUE;
+    if (h->events) {
+        cudaStreamSynchronize(h->stream);
+        for (int i = 0; i < 4 * h->timing_cap; ++i) cudaEventDestroy(h->events[i]);
+        free(h->events);
+        h->events = nullptr;
+    }
+    h->timing_cap = 0;
+    h->timing_count = 0;
+    if (max_calls == 0) return OZIMMU_SUCCESS;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    h->events = static_cast<cudaEvent_t *>(calloc(4 * (size_t)max_calls, sizeof(cudaEvent_t)));
+    if (!h->events) return OZIMMU_ERR_INVALID_VALUE;
+    for (int i = 0; i < 4 * max_calls; ++i)
+        if (cudaEventCreate(&h->events[i]) != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaEventDestroy(h->events[j]);
+            free(h->events);
+            h->events = nullptr;
+            cudaGetLastError();
+            return OZIMMU_ERR_CUDA;
+        }
+    h->timing_cap = max_calls;
+    return OZIMMU_SUCCESS;
+}
+
+int ozimmu_timing_read(ozimmu_handle_t h, ozimmu_timing_t *out, int max_out) {
+    if (!h || (!out && max_out > 0)) return -1;
+    const int n = h->timing_count;
+    for (int c = 0; c < n && c < max_out; ++c) {
+        cudaEvent_t *ev = h->events + 4 * c;
+        float t[3] = {0, 0, 0};
+        for (int p = 0; p < 3; ++p) {
+            if (cudaEventSynchronize(ev[p + 1]) != cudaSuccess ||
+                cudaEventElapsedTime(&t[p], ev[p], ev[p + 1]) != cudaSuccess) {
+                cudaGetLastError();
+                return -1;
+            }
+        }
+        out[c].slice_b_ms = t[0];
+        out[c].slice_a_ms = t[1];
+        out[c].gemm_ms = t[2];
+    }
+    h->timing_count = 0;
+    return n;
+}
+
 ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
     if (!h) return OZIMMU_SUCCESS;
+    if (h->events) {
+        cudaStreamSynchronize(h->stream);
+        for (int i = 0; i < 4 * h->timing_cap; ++i) cudaEventDestroy(h->events[i]);
+        free(h->events);
+    }
     if (h->own_ws) {
         cudaStreamSynchronize(h->stream);
         cudaFree(h->own_ws);
@@ -439,6 +515,7 @@ ozimmu_status_t ozimmu_debug_level_sums(ozimmu_handle_t h, ozimmu_op_t transA,
     ga.w = w;
     ga.out = Lg_out;
     ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
+    ga.wave_counter = reinterpret_cast<unsigned int *>(base + L.sync);
     e = launch_gemm(ga, gp, EPI_LEVELS_I64, h->stream, &launches);
     if (e != cudaSuccess) return cuda_status(e);
     fill_report(h, s, w, m, n, k, &gp, launches, 0);

@@ -48,12 +48,14 @@ struct GemmArgs {
     int64_t ldc;
     void *out;               // EPI_LEVELS_I64: int64 [s][n][m];  EPI_PAIR_I32: int32 [n][m]
     int64_t *chunk_scratch;  // per-CTA partial level sums when k_chunks > 1
+    unsigned int *wave_counter;  // 4-byte device scratch for the soft wave barrier (or null)
 };
 
 struct GemmPlan {
     int tile_n;       // N_c
     int k_block;      // K bytes per stage (= swizzle width)
-    int stages;
+    int stages;       // = a_stages (reported)
+    int a_stages, b_stages;
     int64_t num_k_blocks;
     int64_t chunk_blocks;  // k-blocks per INT32-safe chunk
     int k_chunks;

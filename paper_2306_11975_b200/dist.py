@@ -1,0 +1,86 @@
+"""Multi-GPU Ozaki DGEMM: C partitioned into row blocks, B sliced ONCE and its INT8
+planes broadcast to every rank (BASELINE north_star).
+
+Rank r owns rows [r0, r1) of C and of op(A) and slices its own A rows (row
+exponents are per row -- no communication).  op(B) is sliced on the root only,
+chunk by chunk along n; each chunk's B-slice buffer (INT8 planes + int32 column
+exponents, ozimmu_b_slices_bytes) goes to all ranks with one NCCL broadcast over
+NVLink.  The GEMM on chunk c waits only for chunk c's broadcast, so the transfer
+of chunk c+1 overlaps the tensor-core work on chunk c (NCCL's stream vs the
+compute stream).  There is no reduction: every C element is computed on exactly
+one GPU by the same canonical operation sequence, so C is bitwise identical to the
+single-GPU result for every world size.
+
+The math is done by a backend object (``CudaBackend`` wraps the C ABI); the
+orchestration here is plain torch.distributed and is unit-tested on CPU with
+gloo and a test-only backend.
+"""
+import torch
+import torch.distributed as dist
+
+
+def row_range(m, world, rank):
+    """Balanced contiguous row block [r0, r1) of rank `rank`."""
+    return (m * rank) // world, (m * (rank + 1)) // world
+
+
+def col_chunks(n, chunk_cols):
+    chunk_cols = max(1, int(chunk_cols))
+    return [(c0, min(n, c0 + chunk_cols)) for c0 in range(0, n, chunk_cols)]
+
+
+class CudaBackend:
+    """Backend over libozimmu (device pointers, column-major, stream = current)."""
+
+    def __init__(self, handle, device):
+        self.h = handle
+        self.device = torch.device("cuda", device) if isinstance(device, int) else device
+
+    def b_slices_bytes(self, n, k, s):
+        from .ozimmu import b_slices_bytes
+        return b_slices_bytes(n, k, s)
+
+    def alloc(self, nbytes):
+        return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
+    def bind_stream(self):
+        self.h.set_stream(torch.cuda.current_stream(self.device))
+
+    def slice_b(self, transB, k, c0, c1, B, ldb, s, buf):
+        # column block [c0, c1) of op(B): N -> columns of B; T/C -> rows of B
+        off = c0 * ldb if transB == "N" else c0
+        self.h.slice_b(transB, k, c1 - c0, B.data_ptr() + 8 * off, ldb, s, buf)
+
+    def gemm(self, transA, m_loc, c0, c1, k, alpha, A_loc, lda, buf, beta, C_loc, ldc, s):
+        self.h.dgemm_presliced_b(transA, m_loc, c1 - c0, k, alpha, A_loc, lda, buf, beta,
+                                 C_loc.data_ptr() + 8 * c0 * ldc, ldc, s)
+
+
+def dgemm_rowblock(backend, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta,
+                   C_loc, ldc, s, root=0, chunk_cols=2048, group=None, bufs=None):
+    """C_loc = alpha op(A)[r0:r1] op(B) + beta C_loc on every rank.
+
+    A_loc: this rank's rows of op(A) (stored like A, m_loc rows), C_loc its rows of C.
+    B is only read on `root` (may be None elsewhere).  Returns the list of per-chunk
+    B-slice buffers (reusable via `bufs` to avoid re-allocation)."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    chunks = col_chunks(n, chunk_cols)
+    if bufs is None:
+        bufs = [backend.alloc(backend.b_slices_bytes(c1 - c0, k, s)) for c0, c1 in chunks]
+    works = []
+    # root: slice chunk c, then hand it to NCCL (which orders itself after the slicing
+    # on the current stream) while slicing chunk c+1
+    for (c0, c1), buf in zip(chunks, bufs):
+        if rank == root:
+            backend.slice_b(transB, k, c0, c1, B, ldb, s, buf)
+        if world > 1:
+            works.append(dist.broadcast(buf, src=root, group=group, async_op=True))
+        else:
+            works.append(None)
+    for (c0, c1), buf, w in zip(chunks, bufs, works):
+        if w is not None:
+            w.wait()  # NCCL: the current stream waits for this chunk only
+        if m_loc > 0:
+            backend.gemm(transA, m_loc, c0, c1, k, alpha, A_loc, lda, buf, beta, C_loc, ldc, s)
+    return bufs

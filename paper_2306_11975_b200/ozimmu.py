@@ -26,6 +26,7 @@ EXPORTS = [
     "ozimmu_set_workspace", "ozimmu_get_report", "ozimmu_version", "ozimmu_status_string",
     "ozimmu_dgemm", "ozimmu_b_slices_bytes", "ozimmu_slice_b", "ozimmu_dgemm_presliced_b",
     "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
+    "ozimmu_timing_enable", "ozimmu_timing_read",
 ]
 
 
@@ -33,6 +34,10 @@ class OzimmuError(RuntimeError):
     def __init__(self, fn, code):
         super().__init__(f"{fn} failed: {STATUS.get(code, code)}")
         self.code = code
+
+
+class Timing(ct.Structure):
+    _fields_ = [("slice_b_ms", ct.c_float), ("slice_a_ms", ct.c_float), ("gemm_ms", ct.c_float)]
 
 
 class Report(ct.Structure):
@@ -75,6 +80,8 @@ def lib():
         "ozimmu_debug_split": ([H, i32, i32, i64, i64, vp, i64, i32, vp, vp], i32),
         "ozimmu_debug_level_sums": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, i32, vp], i32),
         "ozimmu_debug_pair": ([H, vp, vp, i64, i64, i64, vp], i32),
+        "ozimmu_timing_enable": ([H, i32], i32),
+        "ozimmu_timing_read": ([H, ct.POINTER(Timing), i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -155,6 +162,17 @@ class Handle:
         r = Report()
         _check("ozimmu_get_report", lib().ozimmu_get_report(self._h, ct.byref(r)))
         return r.as_dict()
+
+    def timing_enable(self, max_calls):
+        _check("ozimmu_timing_enable", lib().ozimmu_timing_enable(self._h, int(max_calls)))
+
+    def timing_read(self, max_out=4096):
+        buf = (Timing * max_out)()
+        n = lib().ozimmu_timing_read(self._h, buf, max_out)
+        if n < 0:
+            raise OzimmuError("ozimmu_timing_read", 4)
+        return [{"slice_b_ms": buf[i].slice_b_ms, "slice_a_ms": buf[i].slice_a_ms,
+                 "gemm_ms": buf[i].gemm_ms} for i in range(min(n, max_out))]
 
     # -- the C ABI, same names and argument order ---------------------------------
     def dgemm(self, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_slices):
