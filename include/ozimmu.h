@@ -90,6 +90,7 @@ typedef struct {
     int stages;            /* SMEM pipeline depth */
     int k_chunks;          /* INT32-overflow-safe K chunks per tile (A4 budget) */
     int launches;          /* kernels launched by the last call */
+    int acc_regions;       /* TMEM accumulator regions per level (INT32 sub-groups of pairs) */
 } ozimmu_report_t;
 
 /* ---- handle ------------------------------------------------------------- */

@@ -3,9 +3,10 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
 #include <cuda_runtime.h>
 
-#include "../../include/ozimmu.h"
+#include "ozimmu.h"
 #include "internal.h"
 
 using namespace ozimmu;
@@ -145,6 +146,7 @@ void fill_report(ozimmu_handle_t h, int s, int w, int64_t m, int64_t n, int64_t 
     r.stages = gp ? gp->stages : 0;
     r.k_chunks = gp ? gp->k_chunks : 0;
     r.launches = launches;
+    r.acc_regions = gp ? gp->T : 0;
 }
 
 // C = beta C (alpha == 0 or k == 0 quick return; A and B are not read).
@@ -231,10 +233,29 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     // soft per-wave grid barrier (L2 reuse); OZIMMU_NO_WAVE_SYNC=1 disables (experiments)
     static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
     ga.wave_counter = no_sync ? nullptr : reinterpret_cast<unsigned int *>(base + L.sync);
+    // development instrumentation: OZIMMU_STATS=1 -> per-CTA stall counters, printed by
+    // ozimmu_debug_print_stats via the environment-only hook below
+    static const bool want_stats = getenv("OZIMMU_STATS") != nullptr;
+    static long long *stats_buf = nullptr;
+    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 8 * 1024 * sizeof(long long));
+    ga.stats = want_stats ? stats_buf : nullptr;
     e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, &launches);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 3);
     mark_done(h);
+    if (ga.stats) {  // development only: synchronous dump of the stall counters
+        long long host[8 * 1024];
+        cudaStreamSynchronize(h->stream);
+        cudaMemcpy(host, ga.stats, sizeof(long long) * 8 * gp.grid, cudaMemcpyDeviceToHost);
+        double acc[8] = {0};
+        for (int c = 0; c < gp.grid; ++c)
+            for (int i = 0; i < 8; ++i) acc[i] += (double)host[c * 8 + i];
+        fprintf(stderr,
+                "[ozimmu stats] grid=%d avg cycles: total=%.0f mma_wait_b=%.0f mma_wait_a=%.0f "
+                "mma_wait_tmem=%.0f prod_wave=%.0f prod_wait_a=%.0f prod_wait_b=%.0f epi_busy=%.0f\n",
+                gp.grid, acc[0] / gp.grid, acc[1] / gp.grid, acc[2] / gp.grid, acc[3] / gp.grid,
+                acc[4] / gp.grid, acc[5] / gp.grid, acc[6] / gp.grid, acc[7] / gp.grid);
+    }
     fill_report(h, s, w, m, n, k, &gp, launches, slice_bytes);
     return OZIMMU_SUCCESS;
 }
@@ -533,6 +554,8 @@ ozimmu_status_t ozimmu_debug_pair(ozimmu_handle_t h, const int8_t *Ai, const int
     if (!plan_gemm(1, 7, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
     gp.chunk_blocks = gp.num_k_blocks;  // caller guarantees the INT32 budget
     gp.k_chunks = 1;
+    gp.T = 1;
+    gp.G = 1;
     const size_t abytes = align_up((size_t)m * k_pad), bbytes = align_up((size_t)n * k_pad);
     void *ws = nullptr;
     ozimmu_status_t st = get_ws(h, abytes + bbytes, &ws);

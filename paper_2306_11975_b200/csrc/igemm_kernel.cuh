@@ -1,0 +1,484 @@
+// igemm_kernel.cuh -- the fused tcgen05 Ozaki GEMM kernel template (see igemm.cu).
+#pragma once
+// Included by igemm.cu (plan + dispatch) and by igemm_inst_*.cu, which hold the explicit
+// instantiations of launch_t<S> (split so nvcc compiles the 32 kernels in parallel).
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace ozimmu {
+namespace gemm_detail {
+
+constexpr int kThreads = 192;  // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int kBlockM = 128;
+constexpr int kKB = 128;       // K bytes per k-block = one 128B swizzle row
+constexpr int kGroupM = 8;     // grouped raster: 8 row-blocks per group
+
+struct KParams {
+    int64_t m, n, k_pad;
+    int s, w;
+    int64_t num_k_blocks, chunk_blocks;
+    int k_chunks;
+    int64_t tiles_m, tiles_n, num_tiles;
+    int a_stages, b_stages;
+    uint32_t a_stage_bytes, b_stage_bytes;
+    uint32_t tmem_cols;
+    int mode;
+    double alpha, beta;
+    const int32_t *EA, *EB;
+    double *C;
+    int64_t ldc;
+    void *out;
+    int64_t *scratch;
+    unsigned int *wave_counter;  // soft grid barrier between tile waves (may be null)
+    int64_t full_waves;          // waves in which every CTA has a tile
+    long long *stats;            // optional per-CTA stall counters (kStatSlots per CTA) or null
+    int G;                       // pairs per INT32 accumulator (sub-group size)
+    int T;                       // accumulator regions (sub-groups) per level, 1 or 2
+    uint32_t region_col[2];      // TMEM column of region t (region t holds levels j < s - tG)
+};
+
+// N_c (output columns per tile) as a function of s: the largest of {64, 48, 32, 16} with
+// s * N_c <= 512 TMEM columns.
+__host__ __device__ constexpr int nc_for(int S) {
+    return S * 64 <= 512 ? 64 : (S * 48 <= 512 ? 48 : (S * 32 <= 512 ? 32 : 16));
+}
+
+// stall-counter slots (development instrumentation, OZIMMU_STATS=1)
+enum : int { ST_TOTAL = 0, ST_MMA_WAIT_B, ST_MMA_WAIT_A, ST_MMA_WAIT_TMEM, ST_PROD_WAVE,
+             ST_PROD_WAIT_A, ST_PROD_WAIT_B, ST_EPI_BUSY, kStatSlots = 8 };
+
+__device__ __forceinline__ void tile_coords(int64_t t, const KParams &P, int64_t &mb,
+                                            int64_t &nb) {
+    const int64_t per_group = (int64_t)kGroupM * P.tiles_n;
+    const int64_t g = t / per_group;
+    const int64_t r = t % per_group;
+    const int64_t gm0 = g * kGroupM;
+    int64_t gsz = P.tiles_m - gm0;
+    gsz = gsz < kGroupM ? gsz : kGroupM;
+    mb = gm0 + r % gsz;
+    nb = r / gsz;
+}
+
+// 2^e as a double for e in the normal range (exact).
+__device__ __forceinline__ double pow2(int e) {
+    return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Soft barrier: CTAs of the persistent grid start tile-wave `wave` together, so that the
+// CTAs sharing A row-blocks / B column-blocks stream the same K range through L2 at the
+// same time.  Bounded wait: never a deadlock if some CTAs are not co-resident.
+__device__ __forceinline__ void wave_sync(const KParams &P, int64_t wave) {
+    if (!P.wave_counter || wave >= P.full_waves) return;
+    atomicAdd(P.wave_counter, 1u);
+    const unsigned int target = (unsigned int)((wave + 1) * gridDim.x);
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire(P.wave_counter) < target) {
+        if (globaltimer() - t0 > 200000ull) break;  // 200 us cap
+        __nanosleep(256);
+    }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const KParams P) {
+    constexpr int NC = nc_for(S);
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // [B ring: b_stages x (s x NC x 128)] [A ring: a_stages x (128 x 128)] [barriers]
+    uint8_t *smB = smem;
+    uint8_t *smA = smem + (size_t)P.b_stages * P.b_stage_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smA + (size_t)P.a_stages * P.a_stage_bytes);
+    uint64_t *b_full = bars;
+    uint64_t *b_empty = b_full + P.b_stages;
+    uint64_t *a_full = b_empty + P.b_stages;
+    uint64_t *a_empty = a_full + P.a_stages;
+    uint64_t *tmem_full = a_empty + P.a_stages;
+    uint64_t *tmem_empty = tmem_full + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 1);
+
+    const uint32_t warp = ptx::warp_id();
+    const uint32_t lane = ptx::lane_id();
+    constexpr int s = S;
+
+    if (warp == 5 && lane == 0) {
+        for (int i = 0; i < P.b_stages; ++i) {
+            ptx::mbar_init(&b_full[i], 1);
+            ptx::mbar_init(&b_empty[i], 1);
+        }
+        for (int i = 0; i < P.a_stages; ++i) {
+            ptx::mbar_init(&a_full[i], 1);
+            ptx::mbar_init(&a_empty[i], 1);
+        }
+        ptx::mbar_init(tmem_full, 1);
+        ptx::mbar_init(tmem_empty, 4 * 32);
+        ptx::fence_mbar_init();
+        ptx::fence_proxy_async();
+    }
+    if (warp == 4 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+    }
+    if (warp == 0) {
+        ptx::tmem_alloc(tmem_slot, P.tmem_cols);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 4) {
+        // ===================== TMA producer =====================
+        if (ptx::elect_one()) {
+            int bs = 0, as = 0;
+            uint32_t bph = 0, aph = 0;
+            int64_t wave = 0;
+            long long st_w = 0, st_pa = 0, st_pb = 0;
+            const uint32_t b_tx = (uint32_t)(s * NC * kKB), a_tx = (uint32_t)(kBlockM * kKB);
+            for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x, ++wave) {
+                int64_t mb, nb;
+                tile_coords(t, P, mb, nb);
+                long long c0 = P.stats ? clock64() : 0;
+                wave_sync(P, wave);
+                if (P.stats) st_w += clock64() - c0;
+                for (int64_t kb = 0; kb < P.num_k_blocks; ++kb) {
+                    long long c1 = P.stats ? clock64() : 0;
+                    ptx::mbar_wait(&b_empty[bs], bph ^ 1);
+                    if (P.stats) st_pb += clock64() - c1;
+                    ptx::mbar_arrive_expect_tx(&b_full[bs], b_tx);
+                    ptx::tma_load_3d(&tmB, &b_full[bs], smB + (size_t)bs * P.b_stage_bytes,
+                                     (int32_t)(kb * kKB), (int32_t)(nb * NC), 0,
+                                     ptx::kEvictNormal);
+                    if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
+                    for (int p = 0; p < s; ++p) {
+                        long long c2 = P.stats ? clock64() : 0;
+                        ptx::mbar_wait(&a_empty[as], aph ^ 1);
+                        if (P.stats) st_pa += clock64() - c2;
+                        ptx::mbar_arrive_expect_tx(&a_full[as], a_tx);
+                        ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
+                                         (int32_t)(kb * kKB), (int32_t)(mb * kBlockM), p,
+                                         ptx::kEvictNormal);
+                        if (++as == P.a_stages) { as = 0; aph ^= 1; }
+                    }
+                }
+            }
+            if (P.stats) {
+                long long *st = P.stats + (int64_t)blockIdx.x * kStatSlots;
+                st[ST_PROD_WAVE] = st_w;
+                st[ST_PROD_WAIT_A] = st_pa;
+                st[ST_PROD_WAIT_B] = st_pb;
+            }
+        }
+    } else if (warp == 5) {
+        // ===================== MMA issuer =====================
+        constexpr int kMaxBlk = 256 / NC;  // window blocks per instruction (N <= 256)
+        // TMEM column of A-slice p's window: region t(p) = (p-1)/G (INT32 sub-group);
+        // the first p of each region initialises it (accumulate = 0).
+        uint32_t pcol[S + 1];
+        uint32_t first_mask = 0;
+#pragma unroll
+        for (int p = 1; p <= S; ++p) {
+            const int t = (p - 1) / P.G;
+            pcol[p] = tmem_base + P.region_col[t];
+            if ((p - 1) % P.G == 0) first_mask |= 1u << p;
+        }
+        int bs = 0, as = 0;
+        uint32_t bph = 0, aph = 0;
+        uint32_t acc_iter = 0;
+        long long st_b = 0, st_a = 0, st_t = 0, t_begin = clock64();
+        const uint64_t adesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smA));
+        const uint64_t bdesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smB));
+        for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+            for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
+                long long c0 = P.stats ? clock64() : 0;
+                ptx::mbar_wait(tmem_empty, (acc_iter & 1) ^ 1);
+                if (P.stats) st_t += clock64() - c0;
+                ptx::tc_fence_after();
+                const int64_t kb0 = (int64_t)c * P.chunk_blocks;
+                int64_t kb1 = kb0 + P.chunk_blocks;
+                kb1 = kb1 < P.num_k_blocks ? kb1 : P.num_k_blocks;
+                for (int64_t kb = kb0; kb < kb1; ++kb) {
+                    long long c1 = P.stats ? clock64() : 0;
+                    ptx::mbar_wait(&b_full[bs], bph);
+                    if (P.stats) st_b += clock64() - c1;
+                    const uint64_t bdesc0 = bdesc_base + ((bs * P.b_stage_bytes) >> 4);
+                    const uint32_t init_mask = kb == kb0 ? first_mask : 0u;
+#pragma unroll
+                    for (int p = 1; p <= S; ++p) {
+                        long long c2 = P.stats ? clock64() : 0;
+                        ptx::mbar_wait(&a_full[as], aph);
+                        if (P.stats) st_a += clock64() - c2;
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            const uint64_t adesc0 = adesc_base + ((as * P.a_stage_bytes) >> 4);
+                            const int L = S + 1 - p;  // window: partners q = 1..L (unrolled: constant)
+#pragma unroll
+                            for (int ks = 0; ks < kKB / 32; ++ks) {
+                                const uint32_t acc = (ks == 0 && ((init_mask >> p) & 1)) ? 0u : 1u;
+#pragma unroll
+                                for (int j0 = 0; j0 < L; j0 += kMaxBlk) {
+                                    const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
+                                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), adesc0 + (uint64_t)(ks * 2),
+                                                bdesc0 + (uint64_t)(((p - 1 + j0) * NC * kKB + ks * 32) >> 4),
+                                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), acc);
+                                }
+                            }
+                            ptx::mma_commit(&a_empty[as]);  // A slot free when these finish
+                        }
+                        __syncwarp();
+                        if (++as == P.a_stages) { as = 0; aph ^= 1; }
+                    }
+                    if (ptx::elect_one()) ptx::mma_commit(&b_empty[bs]);
+                    __syncwarp();
+                    if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
+                }
+                if (ptx::elect_one()) ptx::mma_commit(tmem_full);  // chunk accumulated
+                __syncwarp();
+            }
+        }
+        if (P.stats && lane == 0) {
+            long long *st = P.stats + (int64_t)blockIdx.x * kStatSlots;
+            st[ST_TOTAL] = clock64() - t_begin;
+            st[ST_MMA_WAIT_B] = st_b;
+            st[ST_MMA_WAIT_A] = st_a;
+            st[ST_MMA_WAIT_TMEM] = st_t;
+        }
+    } else {
+        // ===================== epilogue (warps 0-3) =====================
+        // Thread = one row of the tile (TMEM lane).  Per 8-column group: L_g for all levels
+        // (summing the INT32 sub-group regions, plus the int64 partials of earlier K chunks),
+        // then the canonical FP64 combination g = s+1 .. 2 and the store of C.
+        constexpr int kLB = 4;  // levels per batch of TMEM loads (one wait per batch)
+        const uint32_t row_local = warp * 32 + lane;
+        const uint32_t lane_addr = (warp * 32) << 16;
+        int64_t *scr = P.scratch ? P.scratch + (int64_t)blockIdx.x * s * NC * kBlockM : nullptr;
+        const int T = P.T;
+        const int G = P.G;
+        uint32_t acc_iter = 0;
+        long long st_e = 0;
+        for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+            int64_t mb, nb;
+            tile_coords(t, P, mb, nb);
+            const int64_t row = mb * kBlockM + row_local;
+            const bool row_ok = row < P.m;
+            const int32_t ea = (P.mode == EPI_DGEMM && row_ok) ? P.EA[row] : 0;
+            for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
+                ptx::mbar_wait(tmem_full, acc_iter & 1);
+                ptx::tc_fence_after();
+                long long ce = P.stats ? clock64() : 0;
+                const bool first = c == 0, last = c == P.k_chunks - 1;
+#pragma unroll 1
+                for (int cg = 0; cg < NC / 8; ++cg) {
+                    double acc[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+#pragma unroll
+                    for (int j0 = 0; j0 < S; j0 += kLB) {  // levels g = s+1-j, descending g
+                        uint32_t v[kLB][8], v2[kLB][8];
+                        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
+#pragma unroll
+                        for (int jj = 0; jj < kLB; ++jj) {
+                            const int j = j0 + jj;
+                            if (j < S) {
+                                ptx::tmem_ld_x8(tmem_base + lane_addr + P.region_col[0] +
+                                                    (uint32_t)(j * NC + cg * 8), v[jj]);
+                                if (T > 1 && j < S - G)
+                                    ptx::tmem_ld_x8(tmem_base + lane_addr + P.region_col[1] +
+                                                        (uint32_t)(j * NC + cg * 8), v2[jj]);
+                            }
+                        }
+                        int64_t part[kLB][8];
+                        if (scr && !first) {
+#pragma unroll
+                            for (int jj = 0; jj < kLB; ++jj)
+#pragma unroll
+                                for (int i = 0; i < 8; ++i)
+                                    part[jj][i] = (j0 + jj < S) ? scr[((int64_t)((j0 + jj) * NC + cg * 8 + i) * kBlockM) + row_local] : 0;
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < kLB; ++jj)
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) part[jj][i] = 0;
+                        }
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int jj = 0; jj < kLB; ++jj) {
+                            const int j = j0 + jj;
+                            if (j >= S) continue;
+                            int64_t Lg[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                Lg[i] = (int64_t)(int32_t)v[jj][i] + part[jj][i];
+                                if (T > 1 && j < S - G) Lg[i] += (int64_t)(int32_t)v2[jj][i];
+                            }
+                            if (!last) {
+#pragma unroll
+                                for (int i = 0; i < 8; ++i)
+                                    scr[((int64_t)(j * NC + cg * 8 + i) * kBlockM) + row_local] = Lg[i];
+                                continue;
+                            }
+                            if (P.mode == EPI_DGEMM) {
+                                const double sc = pow2(-P.w * (S + 1 - j));
+#pragma unroll
+                                for (int i = 0; i < 8; ++i)
+                                    acc[i] = __dadd_rn(acc[i], __dmul_rn((double)Lg[i], sc));
+                            } else if (row_ok) {
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    const int64_t col = nb * NC + cg * 8 + i;
+                                    if (col >= P.n) continue;
+                                    if (P.mode == EPI_LEVELS_I64) {
+                                        const int gi = S - 1 - j;  // g - 2
+                                        static_cast<int64_t *>(P.out)[(int64_t)gi * P.m * P.n + row +
+                                                                      col * P.m] = Lg[i];
+                                    } else {
+                                        static_cast<int32_t *>(P.out)[row + col * P.m] = (int32_t)Lg[i];
+                                    }
+                                }
+                            }
+                        }
+                    }
+                    if (last && P.mode == EPI_DGEMM && row_ok) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int64_t col = nb * NC + cg * 8 + i;
+                            if (col >= P.n) continue;
+                            const int32_t eb = P.EB[col];
+                            double X;
+                            if (ea == kExpNonFinite || eb == kExpNonFinite)
+                                X = __longlong_as_double(0x7ff8000000000000ll);
+                            else
+                                X = ldexp(acc[i], ea + eb);
+                            double *cp = P.C + row + col * P.ldc;
+                            double r;
+                            if (P.beta == 0.0) r = __dmul_rn(P.alpha, X);
+                            else r = __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
+                            *cp = r;
+                        }
+                    }
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(tmem_empty);
+                if (P.stats) st_e += clock64() - ce;
+            }
+        }
+        if (P.stats && warp == 0 && lane == 0)
+            P.stats[(int64_t)blockIdx.x * kStatSlots + ST_EPI_BUSY] = st_e;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, P.tmem_cols);
+    }
+#endif
+}
+
+// ---- host side -----------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+
+// 3-D map over planes [s][rows][k_pad] (int8, K contiguous), 128B swizzle, box
+// (128 B of K, box_rows rows, box_s slices).
+inline bool make_map(CUtensorMap *map, const int8_t *base, int64_t k_pad, int64_t rows, int s,
+              uint32_t box_rows, uint32_t box_s) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)k_pad, (cuuint64_t)rows, (cuuint64_t)s};
+    cuuint64_t strides[2] = {(cuuint64_t)k_pad, (cuuint64_t)(k_pad * rows)};
+    cuuint32_t box[3] = {(cuuint32_t)kKB, box_rows, box_s};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int S>
+cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st) {
+    constexpr int NC = nc_for(S);
+    CUtensorMap tmA, tmB;
+    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, kBlockM, 1)) return cudaErrorInvalidValue;
+    if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s))
+        return cudaErrorInvalidValue;
+    KParams P;
+    P.m = a.m;
+    P.n = a.n;
+    P.k_pad = a.k_pad;
+    P.s = a.s;
+    P.w = a.w;
+    P.num_k_blocks = p.num_k_blocks;
+    P.chunk_blocks = p.chunk_blocks;
+    P.k_chunks = p.k_chunks;
+    P.tiles_m = ceil_div(a.m, kBlockM);
+    P.tiles_n = ceil_div(a.n, NC);
+    P.num_tiles = P.tiles_m * P.tiles_n;
+    P.a_stages = p.a_stages;
+    P.b_stages = p.b_stages;
+    P.a_stage_bytes = (uint32_t)(kBlockM * kKB);
+    P.b_stage_bytes = (uint32_t)(a.s * NC * kKB);
+    P.tmem_cols = (uint32_t)p.tmem_cols;
+    P.mode = mode;
+    P.alpha = a.alpha;
+    P.beta = a.beta;
+    P.EA = a.EA;
+    P.EB = a.EB;
+    P.C = a.C;
+    P.ldc = a.ldc;
+    P.out = a.out;
+    P.scratch = p.k_chunks > 1 ? a.chunk_scratch : nullptr;
+    P.wave_counter = a.wave_counter;
+    P.stats = a.stats;
+    P.G = p.G;
+    P.T = p.T;
+    P.region_col[0] = 0;
+    P.region_col[1] = (uint32_t)(S * NC);
+    P.full_waves = P.num_tiles / p.grid;
+    if (P.wave_counter) {
+        cudaError_t e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
+        if (e != cudaSuccess) return e;
+    }
+    auto kern = k_oz_gemm<S>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    kern<<<p.grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, P);
+    return cudaGetLastError();
+}
+
+}  // namespace gemm_detail
+}  // namespace ozimmu

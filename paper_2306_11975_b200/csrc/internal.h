@@ -49,6 +49,7 @@ struct GemmArgs {
     void *out;               // EPI_LEVELS_I64: int64 [s][n][m];  EPI_PAIR_I32: int32 [n][m]
     int64_t *chunk_scratch;  // per-CTA partial level sums when k_chunks > 1
     unsigned int *wave_counter;  // 4-byte device scratch for the soft wave barrier (or null)
+    long long *stats;            // optional per-CTA stall counters (development) or null
 };
 
 struct GemmPlan {
@@ -59,6 +60,7 @@ struct GemmPlan {
     int64_t num_k_blocks;
     int64_t chunk_blocks;  // k-blocks per INT32-safe chunk
     int k_chunks;
+    int G, T;          // INT32 sub-groups: T regions of <= G pairs per level
     int grid;
     size_t smem_bytes;
     int tmem_cols;

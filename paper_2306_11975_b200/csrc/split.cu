@@ -7,9 +7,13 @@
 // (P:530); so do we: everything below is integer arithmetic on the IEEE-754 bit
 // pattern, |x| = M * 2^e0 with M the (sub)normal significand.
 //
-// HBM-bound: read 8 B/element (16 B when the rows are strided and need a separate
-// exponent pass), write s B/element.  128-bit loads, 64-bit stores, grids sized
-// in multiples of the SM count.
+// Digit extraction: per element the fixed-point fraction V = floor(|x| 2^(T - E)),
+// T = 32 * ceil(W * S / 32), is built once as 32-bit limbs (a few 64-bit shifts of
+// M); digit p is then bits [T - W p, T - W (p-1)) of V -- one funnel shift and a mask
+// with compile-time amounts -- and the sign is applied as (d ^ m) - m.
+//
+// HBM-bound: read 8 B/element (the strided variant reads twice: exponent pass +
+// transposing slice pass), write s B/element.  128-bit loads, 64-bit stores.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -34,31 +38,84 @@ __device__ __forceinline__ int32_t key_to_exp(int32_t key) {
     return key == kKeyEmpty ? 0 : key;  // all-zero vector: E = 0 (reading A11)
 }
 
-// s digits of x (scale 2^E, width w) packed into out[p] byte `lane` (little endian).
-// Only called with E finite and |x| < 2^E.
-template <int MAXS>
-__device__ __forceinline__ void digits_of(double x, int32_t E, int s, int w, int lane,
-                                          uint64_t (&out)[MAXS]) {
-    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
-    const int be = static_cast<int>((u >> 52) & 0x7FF);
-    const uint64_t fr = u & ((1ull << 52) - 1);
-    const bool neg = (u >> 63) != 0;
-    const uint64_t M = be ? (fr | (1ull << 52)) : fr;  // |x| = M 2^e0
-    const int e0 = be ? be - 1075 : -1074;
-    const int t0 = e0 - E;                              // sh_p = t0 + w p
-    const uint64_t mask = (1ull << w) - 1;
+// floor(M * 2^sh) mod 2^32 for any integer sh (M < 2^53).
+__device__ __forceinline__ uint32_t shifted_limb(uint64_t M, int sh) {
+    uint64_t v;
+    if (sh >= 0) v = sh >= 64 ? 0ull : (M << sh);
+    else v = (-sh) >= 64 ? 0ull : (M >> (-sh));
+    return static_cast<uint32_t>(v);
+}
+
+template <int W, int S>
+struct Digits {
+    static constexpr int NL = (W * S + 31) / 32;  // limbs of the fraction window
+    static constexpr int T = 32 * NL;             // V = floor(|x| 2^(T - E))
+    uint32_t L[NL + 1];
+    uint32_t sm;  // 0 or 0xffffffff (sign of x)
+
+    // x finite, |x| < 2^E (x == 0 gives zero limbs)
+    __device__ __forceinline__ void init(double x, int32_t E) {
+        const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+        const int be = static_cast<int>((u >> 52) & 0x7FF);
+        const uint64_t fr = u & ((1ull << 52) - 1);
+        const uint64_t M = be ? (fr | (1ull << 52)) : fr;  // |x| = M 2^e0
+        const int e0 = be ? be - 1075 : -1074;
+        const int base = e0 - E + T;                         // V = floor(M 2^base)
 #pragma unroll
-    for (int p = 0; p < MAXS; ++p) {
-        if (p < s) {
-            const int sh = t0 + w * (p + 1);
-            uint64_t v;
-            if (sh >= 0) v = sh >= 64 ? 0 : (M << sh);
-            else v = (-sh) >= 64 ? 0 : (M >> (-sh));
-            int d = static_cast<int>(v & mask);
-            d = neg ? -d : d;
-            out[p] |= static_cast<uint64_t>(static_cast<uint8_t>(static_cast<int8_t>(d)))
-                      << (8 * lane);
+        for (int j = 0; j < NL; ++j) L[j] = shifted_limb(M, base - 32 * j);
+        L[NL] = 0;
+        sm = (u >> 63) ? 0xffffffffu : 0u;
+    }
+    // signed digit p (1-based): bits [T - W p, T - W p + W) of V, with the sign of x
+    template <int P>
+    __device__ __forceinline__ uint32_t digit() const {
+        constexpr int t = T - W * P;
+        constexpr int li = t / 32, sh = t % 32;
+        uint32_t d;
+        if (sh + W <= 32) d = (L[li] >> sh) & ((1u << W) - 1);
+        else d = __funnelshift_r(L[li], L[li + 1], sh) & ((1u << W) - 1);
+        return (d ^ sm) - sm;
+    }
+};
+
+// pack the low bytes of 4 words
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    const uint32_t ab = __byte_perm(a, b, 0x0040);
+    const uint32_t cd = __byte_perm(c, d, 0x0040);
+    return __byte_perm(ab, cd, 0x5410);
+}
+
+// Write digit planes p = 1..s of 8 consecutive elements (one 8-byte store per plane).
+template <int W, int S, int P = 1>
+__device__ __forceinline__ void store_digits(const Digits<W, S> (&dg)[8], int s, int reverse,
+                                             int8_t *dst, int64_t plane_stride) {
+    if constexpr (P <= S) {
+        if (P <= s) {
+            uint2 v;
+            v.x = pack4(dg[0].template digit<P>(), dg[1].template digit<P>(),
+                        dg[2].template digit<P>(), dg[3].template digit<P>());
+            v.y = pack4(dg[4].template digit<P>(), dg[5].template digit<P>(),
+                        dg[6].template digit<P>(), dg[7].template digit<P>());
+            const int pidx = reverse ? (s - P) : (P - 1);
+            *reinterpret_cast<uint2 *>(dst + pidx * plane_stride) = v;
+            store_digits<W, S, P + 1>(dg, s, reverse, dst, plane_stride);
         }
+    }
+}
+
+__device__ __forceinline__ void load8(const double *v, int64_t l0, int64_t kdim, bool al16,
+                                      double (&x)[8]) {
+    if (al16 && l0 + 8 <= kdim) {
+        const double2 *q = reinterpret_cast<const double2 *>(v + l0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double2 d2 = __ldg(q + i);
+            x[2 * i] = d2.x;
+            x[2 * i + 1] = d2.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = (l0 + i < kdim) ? __ldg(v + l0 + i) : 0.0;
     }
 }
 
@@ -67,10 +124,10 @@ __device__ __forceinline__ void digits_of(double x, int32_t E, int s, int w, int
 // TPR threads per vector, one pass for the exponent (max reduction), one pass for
 // the digits (the second read of a <= 128 KB row hits L2).
 // ---------------------------------------------------------------------------------
-template <int TPR, int MAXS>
+template <int TPR, int W, int S>
 __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__ M, int64_t ld,
                                                       int64_t rows, int64_t kdim, int64_t k_pad,
-                                                      int s, int w, int reverse,
+                                                      int s, int reverse,
                                                       int8_t *__restrict__ planes,
                                                       int64_t plane_stride, int32_t *__restrict__ E) {
     constexpr int VPB = 256 / TPR;  // vectors per block
@@ -87,20 +144,8 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
     int32_t key = kKeyEmpty;
     if (active) {
         for (int64_t c = t; c < nchunk; c += TPR) {
-            const int64_t l0 = c * 8;
             double x[8];
-            if (al16 && l0 + 8 <= kdim) {
-                const double2 *q = reinterpret_cast<const double2 *>(v + l0);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    double2 d2 = __ldg(q + i);
-                    x[2 * i] = d2.x;
-                    x[2 * i + 1] = d2.y;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) x[i] = (l0 + i < kdim) ? __ldg(v + l0 + i) : 0.0;
-            }
+            load8(v, c * 8, kdim, al16, x);
 #pragma unroll
             for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
         }
@@ -122,34 +167,12 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
     // ---- pass 2: digits ----
     for (int64_t c = t; c < nchunk; c += TPR) {
         const int64_t l0 = c * 8;
-        uint64_t out[MAXS];
+        double x[8];
+        if (!bad) load8(v, l0, kdim, al16, x);
+        Digits<W, S> dg[8];
 #pragma unroll
-        for (int p = 0; p < MAXS; ++p) out[p] = 0;
-        if (!bad) {
-            double x[8];
-            if (al16 && l0 + 8 <= kdim) {
-                const double2 *q = reinterpret_cast<const double2 *>(v + l0);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    double2 d2 = __ldg(q + i);
-                    x[2 * i] = d2.x;
-                    x[2 * i + 1] = d2.y;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) x[i] = (l0 + i < kdim) ? __ldg(v + l0 + i) : 0.0;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-                if (x[i] != 0.0) digits_of<MAXS>(x[i], Ev, s, w, i, out);
-        }
-#pragma unroll
-        for (int p = 0; p < MAXS; ++p) {
-            if (p < s) {
-                const int pidx = reverse ? (s - 1 - p) : p;
-                *reinterpret_cast<uint64_t *>(planes + pidx * plane_stride + r * k_pad + l0) = out[p];
-            }
-        }
+        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
+        store_digits<W, S>(dg, s, reverse, planes + r * k_pad + l0, plane_stride);
     }
 }
 
@@ -180,10 +203,10 @@ __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restric
 }
 
 // Pass 2: 64 vectors x 64 elements per block, transposed through shared memory.
-template <int MAXS>
+template <int W, int S>
 __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict__ M, int64_t ld,
                                                        int64_t rows, int64_t kdim, int64_t k_pad,
-                                                       int s, int w, int reverse,
+                                                       int s, int reverse,
                                                        const int32_t *__restrict__ keys,
                                                        int8_t *__restrict__ planes,
                                                        int64_t plane_stride,
@@ -211,7 +234,7 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
         tile[ll][rr] = (r < rows && l < kdim) ? __ldg(M + r + l * ld) : 0.0;
     }
     __syncthreads();
-#pragma unroll
+#pragma unroll 1
     for (int task = tid; task < 512; task += 256) {
         const int rr = task & 63;
         const int l8 = task >> 6;  // 0..7
@@ -219,40 +242,26 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
         const int64_t lb = l0 + l8 * 8;
         if (r >= rows || lb >= k_pad) continue;
         const int32_t Ev = exps[rr];
-        uint64_t out[MAXS];
+        const bool bad = Ev == kExpNonFinite;
+        Digits<W, S> dg[8];
 #pragma unroll
-        for (int p = 0; p < MAXS; ++p) out[p] = 0;
-        if (Ev != kExpNonFinite) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const double x = tile[l8 * 8 + i][rr];
-                if (x != 0.0) digits_of<MAXS>(x, Ev, s, w, i, out);
-            }
-        }
-#pragma unroll
-        for (int p = 0; p < MAXS; ++p) {
-            if (p < s) {
-                const int pidx = reverse ? (s - 1 - p) : p;
-                *reinterpret_cast<uint64_t *>(planes + pidx * plane_stride + r * k_pad + lb) = out[p];
-            }
-        }
+        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : tile[l8 * 8 + i][rr], bad ? 0 : Ev);
+        store_digits<W, S>(dg, s, reverse, planes + r * k_pad + lb, plane_stride);
     }
 }
 
-template <int MAXS>
+template <int W, int S>
 cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t rows,
-                           int64_t kdim, int64_t k_pad, int s, int w, bool reverse,
-                           int8_t *planes, int64_t plane_stride, int32_t *E,
-                           int32_t *key_scratch, int num_sms, cudaStream_t st, int *launches) {
+                           int64_t kdim, int64_t k_pad, int s, bool reverse, int8_t *planes,
+                           int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
+                           cudaStream_t st, int *launches) {
     if (contiguous) {
         if (k_pad >= 2048) {
-            const int64_t blocks = rows;
-            k_split_contig<256, MAXS><<<(unsigned)blocks, 256, 0, st>>>(
-                M, ld, rows, kdim, k_pad, s, w, reverse, planes, plane_stride, E);
+            k_split_contig<256, W, S><<<(unsigned)rows, 256, 0, st>>>(
+                M, ld, rows, kdim, k_pad, s, reverse, planes, plane_stride, E);
         } else {
-            const int64_t blocks = ceil_div(rows, 8);
-            k_split_contig<32, MAXS><<<(unsigned)blocks, 256, 0, st>>>(
-                M, ld, rows, kdim, k_pad, s, w, reverse, planes, plane_stride, E);
+            k_split_contig<32, W, S><<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(
+                M, ld, rows, kdim, k_pad, s, reverse, planes, plane_stride, E);
         }
         ++*launches;
         return cudaGetLastError();
@@ -271,11 +280,26 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
         M, ld, rows, kdim, lchunk, key_scratch);
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_split_strided<MAXS><<<dim3((unsigned)ceil_div(rows, 64), (unsigned)ceil_div(k_pad, 64)), 256,
-                            0, st>>>(M, ld, rows, kdim, k_pad, s, w, reverse, key_scratch, planes,
+    k_split_strided<W, S><<<dim3((unsigned)ceil_div(rows, 64), (unsigned)ceil_div(k_pad, 64)), 256,
+                            0, st>>>(M, ld, rows, kdim, k_pad, s, reverse, key_scratch, planes,
                                      plane_stride, E);
     ++*launches;
     return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t launch_split_w(const double *M, int64_t ld, bool contiguous, int64_t rows,
+                           int64_t kdim, int64_t k_pad, int s, bool reverse, int8_t *planes,
+                           int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
+                           cudaStream_t st, int *launches) {
+    if (s <= 9)
+        return launch_split_t<W, 9>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
+                                    plane_stride, E, key_scratch, num_sms, st, launches);
+    if (s <= 16)
+        return launch_split_t<W, 16>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
+                                     plane_stride, E, key_scratch, num_sms, st, launches);
+    return launch_split_t<W, 32>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
+                                 plane_stride, E, key_scratch, num_sms, st, launches);
 }
 
 }  // namespace
@@ -285,14 +309,16 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
                          cudaStream_t st, int *launches) {
     if (rows <= 0) return cudaSuccess;
-    if (s <= 8)
-        return launch_split_t<8>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, planes,
-                                 plane_stride, E, key_scratch, num_sms, st, launches);
-    if (s <= 16)
-        return launch_split_t<16>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, planes,
-                                  plane_stride, E, key_scratch, num_sms, st, launches);
-    return launch_split_t<32>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, planes,
-                              plane_stride, E, key_scratch, num_sms, st, launches);
+    if (s < 1 || s > 32) return cudaErrorInvalidValue;
+    switch (w) {
+    case 7: return launch_split_w<7>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
+                                     plane_stride, E, key_scratch, num_sms, st, launches);
+    case 6: return launch_split_w<6>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
+                                     plane_stride, E, key_scratch, num_sms, st, launches);
+    case 5: return launch_split_w<5>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
+                                     plane_stride, E, key_scratch, num_sms, st, launches);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace ozimmu

@@ -44,7 +44,8 @@ class Report(ct.Structure):
     _fields_ = [("num_slices", ct.c_int), ("slice_width", ct.c_int),
                 ("gemm_pairs", ct.c_int64), ("int8_macs", ct.c_int64),
                 ("slice_bytes", ct.c_int64), ("tile_n", ct.c_int), ("k_block", ct.c_int),
-                ("stages", ct.c_int), ("k_chunks", ct.c_int), ("launches", ct.c_int)]
+                ("stages", ct.c_int), ("k_chunks", ct.c_int), ("launches", ct.c_int),
+                ("acc_regions", ct.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
