@@ -237,24 +237,26 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     // ozimmu_debug_print_stats via the environment-only hook below
     static const bool want_stats = getenv("OZIMMU_STATS") != nullptr;
     static long long *stats_buf = nullptr;
-    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 8 * 1024 * sizeof(long long));
+    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 12 * 1024 * sizeof(long long));
     ga.stats = want_stats ? stats_buf : nullptr;
     e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, &launches);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 3);
     mark_done(h);
     if (ga.stats) {  // development only: synchronous dump of the stall counters
-        long long host[8 * 1024];
+        constexpr int NS = 12;
+        static long long host[NS * 1024];
         cudaStreamSynchronize(h->stream);
-        cudaMemcpy(host, ga.stats, sizeof(long long) * 8 * gp.grid, cudaMemcpyDeviceToHost);
-        double acc[8] = {0};
+        cudaMemcpy(host, ga.stats, sizeof(long long) * NS * gp.grid, cudaMemcpyDeviceToHost);
+        double acc[NS] = {0};
         for (int c = 0; c < gp.grid; ++c)
-            for (int i = 0; i < 8; ++i) acc[i] += (double)host[c * 8 + i];
-        fprintf(stderr,
-                "[ozimmu stats] grid=%d avg cycles: total=%.0f mma_wait_b=%.0f mma_wait_a=%.0f "
-                "mma_wait_tmem=%.0f prod_wave=%.0f prod_wait_a=%.0f prod_wait_b=%.0f epi_busy=%.0f\n",
-                gp.grid, acc[0] / gp.grid, acc[1] / gp.grid, acc[2] / gp.grid, acc[3] / gp.grid,
-                acc[4] / gp.grid, acc[5] / gp.grid, acc[6] / gp.grid, acc[7] / gp.grid);
+            for (int i = 0; i < NS; ++i) acc[i] += (double)host[c * NS + i];
+        const char *names[NS] = {"total", "mma_wait_b", "mma_wait_a", "mma_wait_tmem", "prod_wave",
+                                 "prod_wait_a", "prod_wait_b", "epi_busy", "epi_tmem", "epi_store",
+                                 "mma_wait_a_first_kb", "mma_wait_b_kb0"};
+        fprintf(stderr, "[ozimmu stats] grid=%d avg cycles:", gp.grid);
+        for (int i = 0; i < NS; ++i) fprintf(stderr, " %s=%.0f", names[i], acc[i] / gp.grid);
+        fprintf(stderr, "\n");
     }
     fill_report(h, s, w, m, n, k, &gp, launches, slice_bytes);
     return OZIMMU_SUCCESS;

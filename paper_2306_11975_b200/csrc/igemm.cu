@@ -23,6 +23,8 @@
 //  * Epilogue (4 warps, TMEM lane quarter = warp % 4): L_g -> FP64 in the canonical
 //    order g = s+1 .. 2 (reading A6), ldexp by E_A+E_B (A7), alpha/beta (A8), NaN rows (A9),
 //    coalesced column-major stores of C.
+#include <cstdlib>
+
 #include "igemm_kernel.cuh"
 
 namespace ozimmu {
@@ -42,13 +44,16 @@ OZ_EXTERN(27) OZ_EXTERN(28) OZ_EXTERN(29) OZ_EXTERN(30) OZ_EXTERN(31) OZ_EXTERN(
 bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, GemmPlan *p) {
     if (s < 1 || s > 32 || w < 1) return false;
     const int nc = nc_for(s);
-    const size_t smem_budget = 232448 - 2048;  // 227 KB opt-in max minus barriers/alignment
+    const size_t smem_budget = 232448 - 3072;  // 227 KB opt-in max minus barriers/align/static
     const size_t b_stage = (size_t)s * nc * kKB;
     const size_t a_stage = (size_t)kBlockM * kKB;
-    const int b_stages = 2;
+    static const char *bs_env = getenv("OZIMMU_B_STAGES");  // experiments
+    static const char *as_env = getenv("OZIMMU_A_STAGES");
+    const int b_stages = bs_env ? atoi(bs_env) : 2;
     if (b_stages * b_stage + 2 * a_stage > smem_budget) return false;
     int a_stages = (int)((smem_budget - b_stages * b_stage) / a_stage);
     if (a_stages > 12) a_stages = 12;
+    if (as_env && atoi(as_env) >= 2 && atoi(as_env) < a_stages) a_stages = atoi(as_env);
     // INT32 budget: an accumulator holding `g` pair products over K' values of k
     // needs g * K' * (2^w - 1)^2 <= 2^31 - 1.  Level g = s+1 has s pairs.  Prefer splitting the
     // pairs of a level over T = 2 TMEM regions (sub-groups of G pairs) over draining K chunks.
@@ -72,6 +77,8 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     }
     p->tile_n = nc;
     p->k_block = kKB;
+    static const char *pf_env = getenv("OZIMMU_PREFETCH_KB");  // experiments
+    p->prefetch_kb = pf_env ? atoi(pf_env) : 0;  // measured: L2 prefetch slows the B ring
     p->a_stages = a_stages;
     p->b_stages = b_stages;
     p->stages = a_stages;

@@ -36,6 +36,7 @@ struct KParams {
     unsigned int *wave_counter;  // soft grid barrier between tile waves (may be null)
     int64_t full_waves;          // waves in which every CTA has a tile
     long long *stats;            // optional per-CTA stall counters (kStatSlots per CTA) or null
+    int prefetch_kb;             // L2 prefetch distance in k-blocks (0 = off)
     int G;                       // pairs per INT32 accumulator (sub-group size)
     int T;                       // accumulator regions (sub-groups) per level, 1 or 2
     uint32_t region_col[2];      // TMEM column of region t (region t holds levels j < s - tG)
@@ -49,7 +50,8 @@ __host__ __device__ constexpr int nc_for(int S) {
 
 // stall-counter slots (development instrumentation, OZIMMU_STATS=1)
 enum : int { ST_TOTAL = 0, ST_MMA_WAIT_B, ST_MMA_WAIT_A, ST_MMA_WAIT_TMEM, ST_PROD_WAVE,
-             ST_PROD_WAIT_A, ST_PROD_WAIT_B, ST_EPI_BUSY, kStatSlots = 8 };
+             ST_PROD_WAIT_A, ST_PROD_WAIT_B, ST_EPI_BUSY, ST_EPI_TMEM, ST_EPI_STORE,
+             ST_MMA_FIRST_A, ST_MMA_B_TILE0, kStatSlots = 12 };
 
 __device__ __forceinline__ void tile_coords(int64_t t, const KParams &P, int64_t &mb,
                                             int64_t &nb) {
@@ -96,8 +98,9 @@ __device__ __forceinline__ void wave_sync(const KParams &P, int64_t wave) {
 template <int S>
 __global__ void __launch_bounds__(kThreads, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const KParams P) {
+              const __grid_constant__ CUtensorMap tmApf, const KParams P) {
     constexpr int NC = nc_for(S);
+    __shared__ int32_t eb_s[2][64];  // column exponents of the current tile (double-buffered)
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -135,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 4 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
+        ptx::tma_prefetch_desc(&tmApf);
     }
     if (warp == 0) {
         ptx::tmem_alloc(tmem_slot, P.tmem_cols);
@@ -145,6 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+
     if (warp == 4) {
         // ===================== TMA producer =====================
         if (ptx::elect_one()) {
@@ -153,13 +158,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t wave = 0;
             long long st_w = 0, st_pa = 0, st_pb = 0;
             const uint32_t b_tx = (uint32_t)(s * NC * kKB), a_tx = (uint32_t)(kBlockM * kKB);
+            constexpr int kPfS = S < 8 ? S : 8;  // slices per L2-prefetch box
+            auto prefetch = [&](int64_t kb, int64_t mb, int64_t nb) {
+                const int32_t kc = (int32_t)(kb * kKB);
+                ptx::tma_prefetch_l2_3d(&tmB, kc, (int32_t)(nb * NC), 0);
+#pragma unroll
+                for (int z = 0; z < S; z += kPfS)
+                    ptx::tma_prefetch_l2_3d(&tmApf, kc, (int32_t)(mb * kBlockM), z);
+            };
             for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x, ++wave) {
                 int64_t mb, nb;
                 tile_coords(t, P, mb, nb);
                 long long c0 = P.stats ? clock64() : 0;
                 wave_sync(P, wave);
                 if (P.stats) st_w += clock64() - c0;
+                for (int64_t kb = 0; kb < P.prefetch_kb && kb < P.num_k_blocks; ++kb)
+                    prefetch(kb, mb, nb);
                 for (int64_t kb = 0; kb < P.num_k_blocks; ++kb) {
+                    if (P.prefetch_kb && kb + P.prefetch_kb < P.num_k_blocks)
+                        prefetch(kb + P.prefetch_kb, mb, nb);
                     long long c1 = P.stats ? clock64() : 0;
                     ptx::mbar_wait(&b_empty[bs], bph ^ 1);
                     if (P.stats) st_pb += clock64() - c1;
@@ -168,14 +185,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      (int32_t)(kb * kKB), (int32_t)(nb * NC), 0,
                                      ptx::kEvictNormal);
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
-                    for (int p = 0; p < s; ++p) {
+#pragma unroll 1
+                    for (int i = 0; i < S; ++i) {
                         long long c2 = P.stats ? clock64() : 0;
                         ptx::mbar_wait(&a_empty[as], aph ^ 1);
                         if (P.stats) st_pa += clock64() - c2;
                         ptx::mbar_arrive_expect_tx(&a_full[as], a_tx);
                         ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
-                                         (int32_t)(kb * kKB), (int32_t)(mb * kBlockM), p,
-                                         ptx::kEvictNormal);
+                                         (int32_t)(kb * kKB), (int32_t)(mb * kBlockM),
+                                         i, ptx::kEvictNormal);
                         if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
                 }
@@ -190,67 +208,126 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 5) {
         // ===================== MMA issuer =====================
         constexpr int kMaxBlk = 256 / NC;  // window blocks per instruction (N <= 256)
-        // TMEM column of A-slice p's window: region t(p) = (p-1)/G (INT32 sub-group);
-        // the first p of each region initialises it (accumulate = 0).
+        // TMEM column of A-slice p's window: region t(p) = (p-1)/G (INT32 sub-group).
+        // In the first k-block of a period a window's blocks [0, x) were already written by
+        // an earlier window of the same region; blocks [x, L) are new (accumulate = 0).
         uint32_t pcol[S + 1];
-        uint32_t first_mask = 0;
+        int xinit[S + 1];
+        {
+            int seen[2] = {0, 0};
 #pragma unroll
-        for (int p = 1; p <= S; ++p) {
-            const int t = (p - 1) / P.G;
-            pcol[p] = tmem_base + P.region_col[t];
-            if ((p - 1) % P.G == 0) first_mask |= 1u << p;
+            for (int i = 0; i < S; ++i) {
+                const int p = i + 1;
+                const int t = (p - 1) / P.G;
+                pcol[p] = tmem_base + P.region_col[t];
+                const int L = S + 1 - p;
+                xinit[p] = seen[t];
+                seen[t] = seen[t] > L ? seen[t] : L;
+            }
         }
         int bs = 0, as = 0;
         uint32_t bph = 0, aph = 0;
         uint32_t acc_iter = 0;
-        long long st_b = 0, st_a = 0, st_t = 0, t_begin = clock64();
+        long long st_b = 0, st_b0 = 0, st_a = 0, st_t = 0, st_af = 0, t_begin = clock64();
         const uint64_t adesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smA));
         const uint64_t bdesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smB));
+
+        // MMAs of A-slice p for one k-step against its window [0, L) (blocks [x, L) are
+        // initialised when init).
+        auto issue = [&](int p, uint64_t ad, uint64_t bd, bool init, int x) {
+            const int L = S + 1 - p;
+            if (init) {
+                for (int j0 = 0; j0 < x; j0 += kMaxBlk) {
+                    const int nbk = (x - j0) < kMaxBlk ? (x - j0) : kMaxBlk;
+                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad,
+                                bd + (uint64_t)((j0 * NC * kKB) >> 4),
+                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 1u);
+                }
+                for (int j0 = x; j0 < L; j0 += kMaxBlk) {
+                    const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
+                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad,
+                                bd + (uint64_t)((j0 * NC * kKB) >> 4),
+                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 0u);
+                }
+            } else {
+#pragma unroll
+                for (int j0 = 0; j0 < L; j0 += kMaxBlk) {
+                    const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
+                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad,
+                                bd + (uint64_t)((j0 * NC * kKB) >> 4),
+                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 1u);
+                }
+            }
+        };
+
         for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
             for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
-                long long c0 = P.stats ? clock64() : 0;
-                ptx::mbar_wait(tmem_empty, (acc_iter & 1) ^ 1);
-                if (P.stats) st_t += clock64() - c0;
-                ptx::tc_fence_after();
                 const int64_t kb0 = (int64_t)c * P.chunk_blocks;
                 int64_t kb1 = kb0 + P.chunk_blocks;
                 kb1 = kb1 < P.num_k_blocks ? kb1 : P.num_k_blocks;
                 for (int64_t kb = kb0; kb < kb1; ++kb) {
                     long long c1 = P.stats ? clock64() : 0;
                     ptx::mbar_wait(&b_full[bs], bph);
-                    if (P.stats) st_b += clock64() - c1;
+                    if (P.stats) {
+                        if (kb == 0) st_b0 += clock64() - c1;
+                        else st_b += clock64() - c1;
+                    }
                     const uint64_t bdesc0 = bdesc_base + ((bs * P.b_stage_bytes) >> 4);
-                    const uint32_t init_mask = kb == kb0 ? first_mask : 0u;
-#pragma unroll
-                    for (int p = 1; p <= S; ++p) {
-                        long long c2 = P.stats ? clock64() : 0;
-                        ptx::mbar_wait(&a_full[as], aph);
-                        if (P.stats) st_a += clock64() - c2;
+                    if (kb == kb0) {
+                        // ---- first k-block of the period: wait for the epilogue to release
+                        // the accumulator, initialise TMEM blocks on first write ----
+                        long long c0 = P.stats ? clock64() : 0;
+                        ptx::mbar_wait(tmem_empty, (acc_iter & 1) ^ 1);
+                        if (P.stats) st_t += clock64() - c0;
                         ptx::tc_fence_after();
-                        if (ptx::elect_one()) {
-                            const uint64_t adesc0 = adesc_base + ((as * P.a_stage_bytes) >> 4);
-                            const int L = S + 1 - p;  // window: partners q = 1..L (unrolled: constant)
 #pragma unroll
-                            for (int ks = 0; ks < kKB / 32; ++ks) {
-                                const uint32_t acc = (ks == 0 && ((init_mask >> p) & 1)) ? 0u : 1u;
+                        for (int i = 0; i < S; ++i) {
+                            const int p = i + 1;
+                            const int L = S + 1 - p;
+                            long long c2 = P.stats ? clock64() : 0;
+                            ptx::mbar_wait(&a_full[as], aph);
+                            if (P.stats) st_af += clock64() - c2;
+                            ptx::tc_fence_after();
+                            if (ptx::elect_one()) {
+                                const uint64_t adesc0 = adesc_base + ((as * P.a_stage_bytes) >> 4);
+                                const int x = xinit[p] < L ? xinit[p] : L;
 #pragma unroll
-                                for (int j0 = 0; j0 < L; j0 += kMaxBlk) {
-                                    const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
-                                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), adesc0 + (uint64_t)(ks * 2),
-                                                bdesc0 + (uint64_t)(((p - 1 + j0) * NC * kKB + ks * 32) >> 4),
-                                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), acc);
-                                }
+                                for (int ks = 0; ks < kKB / 32; ++ks)
+                                    issue(p, adesc0 + (uint64_t)(ks * 2),
+                                          bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4),
+                                          ks == 0, x);
+                                ptx::mma_commit(&a_empty[as]);
                             }
-                            ptx::mma_commit(&a_empty[as]);  // A slot free when these finish
+                            __syncwarp();
+                            if (++as == P.a_stages) { as = 0; aph ^= 1; }
                         }
-                        __syncwarp();
-                        if (++as == P.a_stages) { as = 0; aph ^= 1; }
+                    } else {
+                        // ---- steady state: ascending p, fully unrolled ----
+#pragma unroll
+                        for (int i = 0; i < S; ++i) {
+                            const int p = i + 1;
+                            long long c2 = P.stats ? clock64() : 0;
+                            ptx::mbar_wait(&a_full[as], aph);
+                            if (P.stats) st_a += clock64() - c2;
+                            ptx::tc_fence_after();
+                            if (ptx::elect_one()) {
+                                const uint64_t adesc0 = adesc_base + ((as * P.a_stage_bytes) >> 4);
+#pragma unroll
+                                for (int ks = 0; ks < kKB / 32; ++ks)
+                                    issue(p, adesc0 + (uint64_t)(ks * 2),
+                                          bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4),
+                                          false, 0);
+                                ptx::mma_commit(&a_empty[as]);
+                            }
+                            __syncwarp();
+                            if (++as == P.a_stages) { as = 0; aph ^= 1; }
+                        }
                     }
                     if (ptx::elect_one()) ptx::mma_commit(&b_empty[bs]);
                     __syncwarp();
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
                 }
-                if (ptx::elect_one()) ptx::mma_commit(tmem_full);  // chunk accumulated
+                if (ptx::elect_one()) ptx::mma_commit(tmem_full);  // period accumulated
                 __syncwarp();
             }
         }
@@ -260,128 +337,196 @@ __global__ void __launch_bounds__(kThreads, 1)
             st[ST_MMA_WAIT_B] = st_b;
             st[ST_MMA_WAIT_A] = st_a;
             st[ST_MMA_WAIT_TMEM] = st_t;
+            st[ST_MMA_FIRST_A] = st_af;
+            st[ST_MMA_B_TILE0] = st_b0;
         }
     } else {
         // ===================== epilogue (warps 0-3) =====================
-        // Thread = one row of the tile (TMEM lane).  Per 8-column group: L_g for all levels
-        // (summing the INT32 sub-group regions, plus the int64 partials of earlier K chunks),
-        // then the canonical FP64 combination g = s+1 .. 2 and the store of C.
-        constexpr int kLB = 4;  // levels per batch of TMEM loads (one wait per batch)
+        // Thread = one row of the tile (TMEM lane).  Level-major: level j (g = s+1-j) of all
+        // NC columns is read from TMEM (both INT32 sub-group regions) and combined in FP64 in
+        // the canonical order g = s+1 .. 2 (reading A6).  The accumulator is released to the
+        // next period's MMAs as soon as every level has been read; the scaling (A7),
+        // alpha/beta (A8), NaN rows/cols (A9) and the stores of C then overlap those MMAs.
         const uint32_t row_local = warp * 32 + lane;
         const uint32_t lane_addr = (warp * 32) << 16;
         int64_t *scr = P.scratch ? P.scratch + (int64_t)blockIdx.x * s * NC * kBlockM : nullptr;
         const int T = P.T;
         const int G = P.G;
-        uint32_t acc_iter = 0;
-        long long st_e = 0;
+        constexpr int kCH = NC < 32 ? NC : 32;  // columns per TMEM read batch
+        uint32_t acc_iter = 0, tile_iter = 0;
+        long long st_e = 0, st_et = 0, st_es = 0;
         for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
             int64_t mb, nb;
             tile_coords(t, P, mb, nb);
             const int64_t row = mb * kBlockM + row_local;
             const bool row_ok = row < P.m;
             const int32_t ea = (P.mode == EPI_DGEMM && row_ok) ? P.EA[row] : 0;
+            // stage this tile's column exponents in shared memory while the MMAs run
+            int32_t *ebt = eb_s[tile_iter & 1];
+            if (P.mode == EPI_DGEMM && row_local < (uint32_t)NC) {
+                const int64_t col = nb * NC + row_local;
+                ebt[row_local] = col < P.n ? P.EB[col] : 0;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            ++tile_iter;
             for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
                 ptx::mbar_wait(tmem_full, acc_iter & 1);
                 ptx::tc_fence_after();
                 long long ce = P.stats ? clock64() : 0;
                 const bool first = c == 0, last = c == P.k_chunks - 1;
+                if (P.mode == EPI_DGEMM && !scr) {
+                    // ---------------- fast path: one period, FP64 result ----------------
+                    double acc[NC];
+#pragma unroll
+                    for (int i = 0; i < NC; ++i) acc[i] = 0.0;
 #pragma unroll 1
-                for (int cg = 0; cg < NC / 8; ++cg) {
-                    double acc[8];
+                    for (int j = 0; j < S; ++j) {  // level g = s+1-j, descending g
+                        const double sc = pow2(-P.w * (S + 1 - j));
+                        const bool two = T > 1 && j < S - G;
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+                        for (int c0 = 0; c0 < NC; c0 += kCH) {
+                            uint32_t v[kCH], v2[kCH];
+                            __syncwarp();
 #pragma unroll
-                    for (int j0 = 0; j0 < S; j0 += kLB) {  // levels g = s+1-j, descending g
-                        uint32_t v[kLB][8], v2[kLB][8];
-                        __syncwarp();  // tcgen05.ld is .sync.aligned: reconverge first
+                            for (int c16 = 0; c16 < kCH; c16 += 16)
+                                if (c0 + c16 < NC)
+                                    ptx::tmem_ld_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16),
+                                                     &v[c16]);
+                            if (two) {
 #pragma unroll
-                        for (int jj = 0; jj < kLB; ++jj) {
-                            const int j = j0 + jj;
-                            if (j < S) {
-                                ptx::tmem_ld_x8(tmem_base + lane_addr + P.region_col[0] +
-                                                    (uint32_t)(j * NC + cg * 8), v[jj]);
-                                if (T > 1 && j < S - G)
-                                    ptx::tmem_ld_x8(tmem_base + lane_addr + P.region_col[1] +
-                                                        (uint32_t)(j * NC + cg * 8), v2[jj]);
-                            }
-                        }
-                        int64_t part[kLB][8];
-                        if (scr && !first) {
+                                for (int c16 = 0; c16 < kCH; c16 += 16)
+                                    if (c0 + c16 < NC)
+                                        ptx::tmem_ld_x16(tmem_base + lane_addr + P.region_col[1] +
+                                                             (uint32_t)(j * NC + c0 + c16), &v2[c16]);
+                                ptx::tmem_ld_wait();
+                                // acc += L_g 2^(-wg): the product is exact, so the fma rounds
+                                // once like the oracle's add; both INT32 parts and their sum
+                                // are exact in binary64.
 #pragma unroll
-                            for (int jj = 0; jj < kLB; ++jj)
+                                for (int ii = 0; ii < kCH; ++ii)
+                                    if (c0 + ii < NC)
+                                        acc[c0 + ii] = __fma_rn(__dadd_rn((double)(int32_t)v[ii],
+                                                                          (double)(int32_t)v2[ii]),
+                                                                sc, acc[c0 + ii]);
+                            } else {
+                                ptx::tmem_ld_wait();
 #pragma unroll
-                                for (int i = 0; i < 8; ++i)
-                                    part[jj][i] = (j0 + jj < S) ? scr[((int64_t)((j0 + jj) * NC + cg * 8 + i) * kBlockM) + row_local] : 0;
-                        } else {
-#pragma unroll
-                            for (int jj = 0; jj < kLB; ++jj)
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) part[jj][i] = 0;
-                        }
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int jj = 0; jj < kLB; ++jj) {
-                            const int j = j0 + jj;
-                            if (j >= S) continue;
-                            int64_t Lg[8];
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                Lg[i] = (int64_t)(int32_t)v[jj][i] + part[jj][i];
-                                if (T > 1 && j < S - G) Lg[i] += (int64_t)(int32_t)v2[jj][i];
-                            }
-                            if (!last) {
-#pragma unroll
-                                for (int i = 0; i < 8; ++i)
-                                    scr[((int64_t)(j * NC + cg * 8 + i) * kBlockM) + row_local] = Lg[i];
-                                continue;
-                            }
-                            if (P.mode == EPI_DGEMM) {
-                                const double sc = pow2(-P.w * (S + 1 - j));
-#pragma unroll
-                                for (int i = 0; i < 8; ++i)
-                                    acc[i] = __dadd_rn(acc[i], __dmul_rn((double)Lg[i], sc));
-                            } else if (row_ok) {
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    const int64_t col = nb * NC + cg * 8 + i;
-                                    if (col >= P.n) continue;
-                                    if (P.mode == EPI_LEVELS_I64) {
-                                        const int gi = S - 1 - j;  // g - 2
-                                        static_cast<int64_t *>(P.out)[(int64_t)gi * P.m * P.n + row +
-                                                                      col * P.m] = Lg[i];
-                                    } else {
-                                        static_cast<int32_t *>(P.out)[row + col * P.m] = (int32_t)Lg[i];
-                                    }
-                                }
+                                for (int ii = 0; ii < kCH; ++ii)
+                                    if (c0 + ii < NC)
+                                        acc[c0 + ii] = __fma_rn((double)(int32_t)v[ii], sc, acc[c0 + ii]);
                             }
                         }
                     }
-                    if (last && P.mode == EPI_DGEMM && row_ok) {
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(tmem_empty);  // accumulator free: next period may start
+                    if (P.stats) st_et += clock64() - ce;
+                    long long cs0 = P.stats ? clock64() : 0;
+                    if (row_ok) {
+                        double *crow = P.C + row;
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int64_t col = nb * NC + cg * 8 + i;
-                            if (col >= P.n) continue;
-                            const int32_t eb = P.EB[col];
+                        for (int i = 0; i < NC; ++i) {
+                            const int64_t col = nb * NC + i;
+                            if (col >= P.n) break;
+                            const int32_t eb = ebt[i];
+                            const int e = ea + eb;
                             double X;
                             if (ea == kExpNonFinite || eb == kExpNonFinite)
                                 X = __longlong_as_double(0x7ff8000000000000ll);
+                            else if (e >= -1022 && e <= 1023)
+                                X = __dmul_rn(acc[i], pow2(e));  // = ldexp: one rounding
                             else
-                                X = ldexp(acc[i], ea + eb);
-                            double *cp = P.C + row + col * P.ldc;
-                            double r;
-                            if (P.beta == 0.0) r = __dmul_rn(P.alpha, X);
-                            else r = __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
-                            *cp = r;
+                                X = ldexp(acc[i], e);
+                            double *cp = crow + col * P.ldc;
+                            *cp = P.beta == 0.0 ? __dmul_rn(P.alpha, X)
+                                                : __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
+                        }
+                    }
+                    if (P.stats) {
+                        st_es += clock64() - cs0;
+                        st_e += clock64() - ce;
+                    }
+                    continue;
+                }
+                // ---------------- general path: K-chunk partials / debug outputs ----------------
+                double acc[NC];
+#pragma unroll
+                for (int i = 0; i < NC; ++i) acc[i] = 0.0;
+#pragma unroll 1
+                for (int j = 0; j < S; ++j) {
+                    const bool two = T > 1 && j < S - G;
+                    const double sc = pow2(-P.w * (S + 1 - j));
+#pragma unroll
+                    for (int c0 = 0; c0 < NC; c0 += kCH) {
+                        uint32_t v[kCH], v2[kCH];
+                        __syncwarp();
+#pragma unroll
+                        for (int c16 = 0; c16 < kCH; c16 += 16) {
+                            if (c0 + c16 >= NC) break;
+                            ptx::tmem_ld_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16),
+                                             &v[c16]);
+                            if (two)
+                                ptx::tmem_ld_x16(tmem_base + lane_addr + P.region_col[1] +
+                                                     (uint32_t)(j * NC + c0 + c16), &v2[c16]);
+                        }
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int ii = 0; ii < kCH; ++ii) {
+                            const int i = c0 + ii;
+                            if (i >= NC) break;
+                            int64_t Lg = (int64_t)(int32_t)v[ii];
+                            if (two) Lg += (int64_t)(int32_t)v2[ii];
+                            if (scr) {
+                                int64_t *sp = scr + ((int64_t)(j * NC + i) * kBlockM) + row_local;
+                                if (!first) Lg += *sp;
+                                if (!last) {
+                                    *sp = Lg;
+                                    continue;
+                                }
+                            }
+                            if (P.mode == EPI_DGEMM) {
+                                acc[i] = __fma_rn((double)Lg, sc, acc[i]);
+                            } else if (row_ok) {
+                                const int64_t col = nb * NC + i;
+                                if (col < P.n) {
+                                    if (P.mode == EPI_LEVELS_I64)
+                                        static_cast<int64_t *>(P.out)[(int64_t)(S - 1 - j) * P.m * P.n +
+                                                                      row + col * P.m] = Lg;
+                                    else
+                                        static_cast<int32_t *>(P.out)[row + col * P.m] = (int32_t)Lg;
+                                }
+                            }
                         }
                     }
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(tmem_empty);
+                if (last && P.mode == EPI_DGEMM && row_ok) {
+#pragma unroll
+                    for (int i = 0; i < NC; ++i) {
+                        const int64_t col = nb * NC + i;
+                        if (col >= P.n) break;
+                        const int32_t eb = ebt[i];
+                        const int e = ea + eb;
+                        double X;
+                        if (ea == kExpNonFinite || eb == kExpNonFinite)
+                            X = __longlong_as_double(0x7ff8000000000000ll);
+                        else if (e >= -1022 && e <= 1023)
+                            X = __dmul_rn(acc[i], pow2(e));
+                        else
+                            X = ldexp(acc[i], e);
+                        double *cp = P.C + row + col * P.ldc;
+                        *cp = P.beta == 0.0 ? __dmul_rn(P.alpha, X)
+                                            : __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
+                    }
+                }
                 if (P.stats) st_e += clock64() - ce;
             }
         }
-        if (P.stats && warp == 0 && lane == 0)
+        if (P.stats && warp == 0 && lane == 0) {
             P.stats[(int64_t)blockIdx.x * kStatSlots + ST_EPI_BUSY] = st_e;
+            P.stats[(int64_t)blockIdx.x * kStatSlots + ST_EPI_TMEM] = st_et;
+            P.stats[(int64_t)blockIdx.x * kStatSlots + ST_EPI_STORE] = st_es;
+        }
     }
     __syncthreads();
     if (warp == 0) {
@@ -435,6 +580,9 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, kBlockM, 1)) return cudaErrorInvalidValue;
     if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s))
         return cudaErrorInvalidValue;
+    CUtensorMap tmApf;  // up to 8 A-slice tiles of a k-block per box (L2 prefetch only)
+    if (!make_map(&tmApf, a.a_planes, a.k_pad, a.m, a.s, kBlockM, (uint32_t)(a.s < 8 ? a.s : 8)))
+        return cudaErrorInvalidValue;
     KParams P;
     P.m = a.m;
     P.n = a.n;
@@ -463,6 +611,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.scratch = p.k_chunks > 1 ? a.chunk_scratch : nullptr;
     P.wave_counter = a.wave_counter;
     P.stats = a.stats;
+    P.prefetch_kb = p.prefetch_kb;
     P.G = p.G;
     P.T = p.T;
     P.region_col[0] = 0;
@@ -476,7 +625,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
     if (e != cudaSuccess) return e;
-    kern<<<p.grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, P);
+    kern<<<p.grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, tmApf, P);
     return cudaGetLastError();
 }
 
