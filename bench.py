@@ -305,9 +305,16 @@ def main():
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    int8_burst = 2.0 * peaks.get("bf16_tflops", int8_peak / 2.0)
+    hw_at_clock = None
+    if clk.get("sm_mhz"):
+        hw_at_clock = 148 * 8192 * 2 * clk["sm_mhz"] * 1e6 / 1e12  # INT8 MAC/clk/SM x 2 ops
     roofline = {"bound": "tensor", "kernel": "k_oz_gemm (tcgen05.mma.kind::i8 + FP64 epilogue)",
                 "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
                 "frac": (achieved / int8_peak) if achieved else None, "traffic": traffic,
+                "frac_of_burst_peak": (achieved / int8_burst) if achieved else None,
+                "tensor_util_at_measured_clock": (achieved / hw_at_clock)
+                if (achieved and hw_at_clock) else None,
                 "ops_per_launch": int8_ops_launch, "ops": "INT8 ops (2 per MAC) = s(s+1) m_loc n k",
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json; {INT8_PEAK_NOTE}",
                 "gemm_ms": gemm_ms, "slice_ms": slice_ms,

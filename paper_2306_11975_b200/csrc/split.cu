@@ -202,7 +202,16 @@ __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restric
     if (key != kKeyEmpty) atomicMax(keys + r, key);
 }
 
-// Pass 2: 64 vectors x 64 elements per block, transposed through shared memory.
+// Pass 2: 32 vectors x 128 elements per block, transposed through shared memory so that
+// both the global reads (32 consecutive vectors at one l) and the plane writes (16 lanes x
+// 8 B = 128 contiguous bytes of one vector) are coalesced.  Shared-memory layout: element
+// (r, l) -> pair q = l/2 stored at pair slot q ^ ((q >> 2) & 7) ^ (r & 7) of row r, which
+// keeps both the column-wise writes and the 16-byte row reads (nearly) conflict-free.
+__device__ __forceinline__ int tslot(int r, int l) {
+    const int q = l >> 1;
+    return 2 * (q ^ ((q >> 2) & 7) ^ (r & 7)) + (l & 1);
+}
+
 template <int W, int S>
 __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict__ M, int64_t ld,
                                                        int64_t rows, int64_t kdim, int64_t k_pad,
@@ -211,12 +220,12 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
                                                        int8_t *__restrict__ planes,
                                                        int64_t plane_stride,
                                                        int32_t *__restrict__ E) {
-    __shared__ double tile[64][65];  // [l][r]
-    __shared__ int32_t exps[64];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
-    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * 64;
+    __shared__ __align__(16) double tile[32][128];  // [r][swizzled l]
+    __shared__ int32_t exps[32];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * 128;
     const int tid = threadIdx.x;
-    if (tid < 64) {
+    if (tid < 32) {
         const int64_t r = r0 + tid;
         int32_t e = 0;
         if (r < rows) {
@@ -226,26 +235,36 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
         exps[tid] = e;
     }
     // coalesced load: warp reads 32 consecutive vectors at one l
+    {
+        const int rr = tid & 31;
+        const int64_t r = r0 + rr;
 #pragma unroll 4
-    for (int i = 0; i < 16; ++i) {
-        const int rr = tid & 63;
-        const int ll = (tid >> 6) + 4 * i;
-        const int64_t r = r0 + rr, l = l0 + ll;
-        tile[ll][rr] = (r < rows && l < kdim) ? __ldg(M + r + l * ld) : 0.0;
+        for (int it = 0; it < 16; ++it) {
+            const int ll = (tid >> 5) + 8 * it;
+            const int64_t l = l0 + ll;
+            tile[rr][tslot(rr, ll)] = (r < rows && l < kdim) ? __ldg(M + r + l * ld) : 0.0;
+        }
     }
     __syncthreads();
 #pragma unroll 1
     for (int task = tid; task < 512; task += 256) {
-        const int rr = task & 63;
-        const int l8 = task >> 6;  // 0..7
+        const int c8 = task & 15;  // 8-element chunk of the row
+        const int rr = task >> 4;  // 0..31
         const int64_t r = r0 + rr;
-        const int64_t lb = l0 + l8 * 8;
+        const int64_t lb = l0 + c8 * 8;
         if (r >= rows || lb >= k_pad) continue;
         const int32_t Ev = exps[rr];
         const bool bad = Ev == kExpNonFinite;
+        double x[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 d2 = *reinterpret_cast<const double2 *>(&tile[rr][tslot(rr, c8 * 8 + 2 * h)]);
+            x[2 * h] = d2.x;
+            x[2 * h + 1] = d2.y;
+        }
         Digits<W, S> dg[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : tile[l8 * 8 + i][rr], bad ? 0 : Ev);
+        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
         store_digits<W, S>(dg, s, reverse, planes + r * k_pad + lb, plane_stride);
     }
 }
@@ -280,7 +299,7 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
         M, ld, rows, kdim, lchunk, key_scratch);
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_split_strided<W, S><<<dim3((unsigned)ceil_div(rows, 64), (unsigned)ceil_div(k_pad, 64)), 256,
+    k_split_strided<W, S><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(k_pad, 128)), 256,
                             0, st>>>(M, ld, rows, kdim, k_pad, s, reverse, key_scratch, planes,
                                      plane_stride, E);
     ++*launches;
