@@ -141,6 +141,24 @@ OZIMMU_API ozimmu_status_t ozimmu_dgemm(ozimmu_handle_t h, ozimmu_op_t transA, o
                              const double *A, int64_t lda, const double *B, int64_t ldb,
                              const double *beta, double *C, int64_t ldc, int num_slices);
 
+/* Complex GEMM (NEXT row f1; "separating the real and imaginary parts ... while
+ * splitting").  Complex numbers are interleaved (re, im) doubles (cuDoubleComplex layout);
+ * lda / ldb / ldc count complex elements; alpha and beta point to 2 doubles (re, im);
+ * OZIMMU_OP_C = conjugate transpose.  Reading A16: the real embedding
+ *   Ahat(i,2l) = Re op(A)(i,l), Ahat(i,2l+1) = Im op(A)(i,l),
+ *   Bhat(:,2j) = (Re, -Im) and Bhat(:,2j+1) = (Im, Re) of op(B)(:,j) interleaved along K,
+ * is computed by the method (s slices, K' = 2k, one shared exponent per complex row of op(A)
+ * and complex column of op(B)); X = Xhat(:,2j) + i Xhat(:,2j+1);
+ * C = alpha X (+ beta C) with z = a x as re = fma(ar, xr, -(ai xi)), im = fma(ar, xi, ai xr).
+ * Effective rate: 8mnk flops. */
+OZIMMU_API ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB,
+                             int64_t m, int64_t n, int64_t k, const double *alpha,
+                             const double *A, int64_t lda, const double *B, int64_t ldb,
+                             const double *beta, double *C, int64_t ldc, int num_slices);
+/* Workspace bytes for ozimmu_zgemm (0 on invalid input). */
+OZIMMU_API size_t ozimmu_zgemm_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
+                                    int64_t n, int64_t k, int num_slices);
+
 /* ---- split-phase entry points (multi-GPU: slice B once, broadcast, reuse) -----
  * A "B-slice buffer" is one contiguous device buffer holding the INT8 planes of
  * the columns of op(B) plus their int32 exponents, in the exact layout the GEMM

@@ -110,3 +110,34 @@ int fp64_gemm_sub(int transA, int transB, int64_t m, int64_t n, int64_t k,
     }
     return 0;
 }
+
+/* Complex DD reference: Re and Im of op(A) op(B) accumulated in DD (each of the four
+ * real products formed exactly by two_prod), ascending l.  Interleaved complex data;
+ * op 2 = conjugate transpose.  Outputs [nr][nc] row-major hi/lo per part. */
+int dd_zgemm_sub(int transA, int transB, int64_t m, int64_t n, int64_t k,
+                 const double *A, int64_t lda, const double *B, int64_t ldb,
+                 const int64_t *ri, int64_t nr, const int64_t *cj, int64_t nc,
+                 double *Rhi, double *Rlo, double *Ihi, double *Ilo)
+{
+    if (m < 0 || n < 0 || k < 0) return 1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t a = 0; a < nr; ++a) {
+        for (int64_t b = 0; b < nc; ++b) {
+            dd_t re = {0.0, 0.0}, im = {0.0, 0.0};
+            for (int64_t l = 0; l < k; ++l) {
+                const double *x = transA == 0 ? &A[2 * (ri[a] + l * lda)] : &A[2 * (l + ri[a] * lda)];
+                const double *y = transB == 0 ? &B[2 * (l + cj[b] * ldb)] : &B[2 * (cj[b] + l * ldb)];
+                const double xr = x[0], xi = transA == 2 ? -x[1] : x[1];
+                const double yr = y[0], yi = transB == 2 ? -y[1] : y[1];
+                dd_t p;
+                dd_two_prod(xr, yr, &p.hi, &p.lo); re = dd_add(re, p);
+                dd_two_prod(-xi, yi, &p.hi, &p.lo); re = dd_add(re, p);
+                dd_two_prod(xr, yi, &p.hi, &p.lo); im = dd_add(im, p);
+                dd_two_prod(xi, yr, &p.hi, &p.lo); im = dd_add(im, p);
+            }
+            Rhi[a * nc + b] = re.hi; Rlo[a * nc + b] = re.lo;
+            Ihi[a * nc + b] = im.hi; Ilo[a * nc + b] = im.lo;
+        }
+    }
+    return 0;
+}

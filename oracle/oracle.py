@@ -42,6 +42,12 @@ def lib():
         L.oz_ref_level_sums_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, i32,
                                             vp, i64, vp, i64, vp]
         L.oz_ref_level_sums_sub.restype = i32
+        L.oz_ref_zgemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, vp, i64, vp, i64, vp, vp,
+                                       i64, i32, vp, i64, vp, i64]
+        L.oz_ref_zgemm_sub.restype = i32
+        L.dd_zgemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
+                                   vp, vp, vp, vp]
+        L.dd_zgemm_sub.restype = i32
         L.dd_two_sum.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
         L.dd_two_prod.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
         L.dd_gemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
@@ -184,6 +190,71 @@ def level_sums(transA, transB, m, n, k, A, lda, B, ldb, s, rows=None, cols=None)
     if rc:
         raise ValueError(f"oz_ref_level_sums_sub failed rc={rc}")
     return out
+
+
+def _c128(a):
+    a = np.asarray(a, dtype=np.complex128)
+    if not (a.flags.f_contiguous or a.flags.c_contiguous):
+        a = np.asfortranarray(a)
+    return a
+
+
+def zgemm(transA, transB, m, n, k, alpha_, A, lda, B, ldb, beta, C, ldc, s, rows=None,
+          cols=None):
+    """Complex Ozaki GEMM (reading A16: real embedding with interleaved K, mode L).
+    A, B, C: complex128 buffers addressed column-major (X[i + j*ld]).  Returns a copy of C."""
+    A = _c128(A)
+    B = _c128(B)
+    Cout = np.array(C, dtype=np.complex128, copy=True, order="K")
+    al = np.array([complex(alpha_).real, complex(alpha_).imag])
+    be = np.array([complex(beta).real, complex(beta).imag])
+    ri, cj = _idx(rows, m), _idx(cols, n)
+    rc = lib().oz_ref_zgemm_sub(OP[transA], OP[transB], m, n, k, _p(al), _p(A), lda, _p(B),
+                                ldb, _p(be), _p(Cout), ldc, int(s), _p(ri), len(ri), _p(cj),
+                                len(cj))
+    if rc:
+        raise ValueError(f"oz_ref_zgemm_sub failed rc={rc}")
+    return Cout
+
+
+def zgemm_simple(A, B, s, alpha_=1.0, beta=0.0, C=None, transA="N", transB="N", rows=None,
+                 cols=None):
+    A = np.asfortranarray(A, dtype=np.complex128)
+    B = np.asfortranarray(B, dtype=np.complex128)
+    m = A.shape[0] if OP[transA] == 0 else A.shape[1]
+    k = A.shape[1] if OP[transA] == 0 else A.shape[0]
+    n = B.shape[1] if OP[transB] == 0 else B.shape[0]
+    if C is None:
+        C = np.zeros((m, n), dtype=np.complex128, order="F")
+    C = np.asfortranarray(C, dtype=np.complex128)
+    return zgemm(transA, transB, m, n, k, alpha_, A, A.shape[0], B, B.shape[0], beta, C, m, s,
+                 rows, cols)
+
+
+def dd_zgemm(transA, transB, m, n, k, A, lda, B, ldb, rows=None, cols=None):
+    """Returns (re_hi, re_lo, im_hi, im_lo) as [nr][nc] arrays."""
+    A = _c128(A)
+    B = _c128(B)
+    ri, cj = _idx(rows, m), _idx(cols, n)
+    out = [np.zeros((len(ri), len(cj))) for _ in range(4)]
+    lib().dd_zgemm_sub(OP[transA], OP[transB], m, n, k, _p(A), lda, _p(B), ldb, _p(ri), len(ri),
+                       _p(cj), len(cj), *[_p(o) for o in out])
+    return tuple(out)
+
+
+def zerr_stats(C, rh, rl, ih, il):
+    """Complex relative error |C - C_DD| / |C_DD| (modulus), as err_stats."""
+    C = np.asarray(C, dtype=np.complex128)
+    dr = (C.real - rh) - rl
+    di = (C.imag - ih) - il
+    diff = np.hypot(dr, di)
+    ref = np.hypot(rh, ih)
+    nz = ref != 0
+    rel = diff[nz] / ref[nz]
+    return {"mean_rel": float(rel.mean()) if rel.size else 0.0,
+            "max_rel": float(rel.max()) if rel.size else 0.0,
+            "nw_max": float(diff.max() / ref.max()) if ref.max() > 0 else float(diff.max()),
+            "zero_ref": int((~nz).sum())}
 
 
 # --- DD reference ------------------------------------------------------------------

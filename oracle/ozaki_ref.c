@@ -327,3 +327,100 @@ int oz_ref_level_sums_sub(int transA, int transB, int64_t m, int64_t n, int64_t 
     free(Ar); free(Bc); free(dA); free(dB); free(EA); free(EB);
     return err;
 }
+
+/* ------------------------------------------------------------------------- */
+/* f1: complex GEMM ("We can compute a complex GEMM by separating   */
+/* the real and imaginary parts ... while splitting").  Reading A16 (DESIGN): */
+/* the real embedding with interleaved K                                       */
+/*   Ahat(i, 2l) = Re op(A)(i,l),   Ahat(i, 2l+1) = Im op(A)(i,l)              */
+/*   Bhat(2l, 2j) = Re op(B)(l,j),  Bhat(2l+1, 2j)   = -Im op(B)(l,j)          */
+/*   Bhat(2l, 2j+1) = Im op(B)(l,j), Bhat(2l+1, 2j+1) = Re op(B)(l,j)          */
+/* so that (Ahat Bhat)(i,2j) = Re(op(A)op(B))(i,j) and (i,2j+1) = Im; the     */
+/* Ozaki method (mode L, K' = 2k) is applied to the real product, i.e. one    */
+/* shared exponent per complex row of op(A) / complex column of op(B).        */
+/* Complex data is interleaved (re, im) doubles; op 2 = conjugate transpose. */
+/* Then with X = Xre + i Xim (reading A8 generalised):                        */
+/*   alpha == 0: C = beta C (complex product below; beta == 0 -> C = 0)       */
+/*   T = alpha X:  Tre = fma(ar, Xre, -(ai*Xim)),  Tim = fma(ar, Xim, ai*Xre)  */
+/*   beta == 0: C = T; else U = beta C_in (same form), C = T + U per part.     */
+/* ------------------------------------------------------------------------- */
+static void cmul(double ar, double ai, double xr, double xi, double *zr, double *zi)
+{
+    double t = ai * xi;
+    *zr = fma(ar, xr, -t);
+    double u = ai * xr;
+    *zi = fma(ar, xi, u);
+}
+
+int oz_ref_zgemm_sub(int transA, int transB, int64_t m, int64_t n, int64_t k,
+                     const double *alpha, const double *A, int64_t lda, const double *B,
+                     int64_t ldb, const double *beta, double *C, int64_t ldc, int s,
+                     const int64_t *ri, int64_t nr, const int64_t *cj, int64_t nc)
+{
+    if (m < 0 || n < 0 || k < 0 || s < 1 || nr < 0 || nc < 0) return OZR_ERR_ARG;
+    if (nr == 0 || nc == 0) return OZR_OK;
+    const int alpha_zero = alpha[0] == 0.0 && alpha[1] == 0.0;
+    const int beta_zero = beta[0] == 0.0 && beta[1] == 0.0;
+    if (alpha_zero || k == 0) {
+        for (int64_t b = 0; b < nc; ++b)
+            for (int64_t a = 0; a < nr; ++a) {
+                double *c = &C[2 * (ri[a] + cj[b] * ldc)];
+                if (beta_zero) { c[0] = 0.0; c[1] = 0.0; }
+                else { double zr, zi; cmul(beta[0], beta[1], c[0], c[1], &zr, &zi); c[0] = zr; c[1] = zi; }
+            }
+        return OZR_OK;
+    }
+    const int64_t K2 = 2 * k;
+    /* Ahat restricted to the selected rows: nr x K2 (row-major), Bhat columns 2j, 2j+1 for
+     * the selected j as a K2 x (2 nc) column-major real matrix. */
+    double *Ah = (double *)malloc(sizeof(double) * (size_t)(nr * K2));
+    double *Bh = (double *)malloc(sizeof(double) * (size_t)(K2 * 2 * nc));
+    double *Xh = (double *)calloc((size_t)(nr * 2 * nc), sizeof(double));
+    int64_t *rr = (int64_t *)malloc(sizeof(int64_t) * (size_t)nr);
+    int64_t *cc = (int64_t *)malloc(sizeof(int64_t) * (size_t)(2 * nc));
+    int err = OZR_ERR_ARG;
+    if (Ah && Bh && Xh && rr && cc) {
+        for (int64_t a = 0; a < nr; ++a) {
+            rr[a] = a;
+            for (int64_t l = 0; l < k; ++l) {
+                const double *z = transA == 0 ? &A[2 * (ri[a] + l * lda)] : &A[2 * (l + ri[a] * lda)];
+                Ah[a * K2 + 2 * l] = z[0];
+                Ah[a * K2 + 2 * l + 1] = transA == 2 ? -z[1] : z[1];
+            }
+        }
+        for (int64_t b = 0; b < nc; ++b) {
+            cc[2 * b] = 2 * b;
+            cc[2 * b + 1] = 2 * b + 1;
+            for (int64_t l = 0; l < k; ++l) {
+                const double *z = transB == 0 ? &B[2 * (l + cj[b] * ldb)] : &B[2 * (cj[b] + l * ldb)];
+                const double re = z[0], im = transB == 2 ? -z[1] : z[1];
+                Bh[(2 * b) * K2 + 2 * l] = re;
+                Bh[(2 * b) * K2 + 2 * l + 1] = -im;
+                Bh[(2 * b + 1) * K2 + 2 * l] = im;
+                Bh[(2 * b + 1) * K2 + 2 * l + 1] = re;
+            }
+        }
+        /* X = Ahat Bhat by the real method (mode L), alpha = 1, beta = 0.
+         * Ahat is row-major nr x K2 = column-major with trans = T, ld = K2. */
+        err = oz_ref_dgemm_sub(1, 0, nr, 2 * nc, K2, 1.0, Ah, K2, Bh, K2, 0.0, Xh, nr, s, 0,
+                               rr, nr, cc, 2 * nc);
+    }
+    if (!err) {
+        for (int64_t b = 0; b < nc; ++b)
+            for (int64_t a = 0; a < nr; ++a) {
+                const double xr = Xh[a + (2 * b) * nr], xi = Xh[a + (2 * b + 1) * nr];
+                double tr, ti;
+                cmul(alpha[0], alpha[1], xr, xi, &tr, &ti);
+                double *c = &C[2 * (ri[a] + cj[b] * ldc)];
+                if (beta_zero) { c[0] = tr; c[1] = ti; }
+                else {
+                    double ur, ui;
+                    cmul(beta[0], beta[1], c[0], c[1], &ur, &ui);
+                    c[0] = tr + ur;
+                    c[1] = ti + ui;
+                }
+            }
+    }
+    free(Ah); free(Bh); free(Xh); free(rr); free(cc);
+    return err;
+}

@@ -108,6 +108,22 @@ inline void mark_done(ozimmu_handle_t h) {
     if (h->timing_cap && h->timing_count < h->timing_cap) ++h->timing_count;
 }
 
+// C = beta C for complex C (interleaved), same product as the ZGEMM epilogue (reading A16).
+__global__ void k_scale_z(double2 *C, int64_t ldc, int64_t m, int64_t n, double br, double bi) {
+    const int64_t total = m * n;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t % m, j = t / m;
+        double2 *c = C + i + j * ldc;
+        if (br == 0.0 && bi == 0.0) {
+            *c = make_double2(0.0, 0.0);
+        } else {
+            const double2 v = *c;
+            *c = make_double2(__fma_rn(br, v.x, -__dmul_rn(bi, v.y)), __fma_rn(br, v.y, __dmul_rn(bi, v.x)));
+        }
+    }
+}
+
 ozimmu_status_t cuda_status(cudaError_t e) {
     if (e == cudaSuccess) return OZIMMU_SUCCESS;
     cudaGetLastError();
@@ -583,6 +599,120 @@ ozimmu_status_t ozimmu_debug_pair(ozimmu_handle_t h, const int8_t *Ai, const int
     e = launch_gemm(ga, gp, EPI_PAIR_I32, h->stream, &launches);
     if (e != cudaSuccess) return cuda_status(e);
     fill_report(h, 1, 7, m, n, k, &gp, launches, 0);
+    return OZIMMU_SUCCESS;
+}
+
+
+// ---- f1: complex GEMM (reading A16: real embedding with interleaved K) -------------------
+
+static size_t zgemm_ws(int64_t m, int64_t n, int64_t k, int s, int num_sms, GemmPlan *gp_out,
+                       Layout *L_out) {
+    const int64_t K2 = 2 * k;
+    const int w = slice_width(K2);
+    const int64_t k_pad = round_up(K2, 16);
+    GemmPlan gp;
+    if (!plan_gemm(s, w, m > 0 ? m : 1, 2 * (n > 0 ? n : 1), k_pad, num_sms, &gp)) return 0;
+    Layout L = layout(m, 2 * n, k_pad, s, chunk_scratch_bytes(gp, s));
+    if (gp_out) *gp_out = gp;
+    if (L_out) *L_out = L;
+    return L.total;
+}
+
+size_t ozimmu_zgemm_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m, int64_t n,
+                                    int64_t k, int num_slices) {
+    if (!valid_op(transA) || !valid_op(transB) || m < 0 || n < 0 || k < 1 || num_slices < 1 ||
+        num_slices > OZIMMU_MAX_SLICES || 2 * k > OZIMMU_MAX_K)
+        return 0;
+    return zgemm_ws(m, n, k, num_slices, 148, nullptr, nullptr);
+}
+
+ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
+                             int64_t n, int64_t k, const double *alpha, const double *A,
+                             int64_t lda, const double *B, int64_t ldb, const double *beta,
+                             double *C, int64_t ldc, int num_slices) {
+    ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc, num_slices);
+    if (st) return st;
+    if (!valid_op(transB)) return OZIMMU_ERR_INVALID_VALUE;
+    const int64_t brows = transB == OZIMMU_OP_N ? k : n;
+    if (ldb < (brows > 1 ? brows : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    const bool alpha0 = alpha[0] == 0.0 && alpha[1] == 0.0;
+    if (n > 0 && k > 0 && m > 0 && !alpha0 && !B) return OZIMMU_ERR_INVALID_VALUE;
+    if (2 * k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    if (m == 0 || n == 0) {
+        fill_report(h, 0, 0, m, n, k, nullptr, 0, 0);
+        return OZIMMU_SUCCESS;
+    }
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    if (alpha0 || k == 0) {
+        int launches = 0;
+        if (!(beta[0] == 1.0 && beta[1] == 0.0)) {
+            int64_t blocks = ceil_div(m * n, 256);
+            if (blocks > 8 * (int64_t)h->num_sms) blocks = 8 * (int64_t)h->num_sms;
+            k_scale_z<<<(unsigned)blocks, 256, 0, h->stream>>>(reinterpret_cast<double2 *>(C), ldc,
+                                                               m, n, beta[0], beta[1]);
+            ++launches;
+            if (cudaGetLastError() != cudaSuccess) return OZIMMU_ERR_CUDA;
+        }
+        fill_report(h, 0, 0, m, n, 0, nullptr, launches, 0);
+        return OZIMMU_SUCCESS;
+    }
+    const int s = num_slices;
+    const int64_t K2 = 2 * k;
+    const int w = slice_width(K2);
+    const int64_t k_pad = round_up(K2, 16);
+    GemmPlan gp;
+    Layout L;
+    if (!zgemm_ws(m, n, k, s, h->num_sms, &gp, &L)) return OZIMMU_ERR_UNSUPPORTED;
+    void *ws = nullptr;
+    if ((st = get_ws(h, L.total, &ws))) return st;
+    uint8_t *base = static_cast<uint8_t *>(ws);
+    int8_t *a_planes = reinterpret_cast<int8_t *>(base + L.a_planes);
+    int32_t *EA = reinterpret_cast<int32_t *>(base + L.a_exp);
+    uint8_t *bbuf = base + L.b_buf;
+    int8_t *b_planes = reinterpret_cast<int8_t *>(bbuf);
+    int32_t *EB = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(2 * n, k_pad, s));
+    int32_t *keys = reinterpret_cast<int32_t *>(base + L.keys);
+    int launches = 0;
+    mark(h, 0);
+    // columns of op(B): contiguous (re, im) pairs iff transB == N -> 2n plane rows
+    const bool bcontig = transB == OZIMMU_OP_N;
+    cudaError_t e = launch_split(B, bcontig ? 2 * ldb : ldb, bcontig, n, K2, k_pad, s, w,
+                                 /*reverse=*/true, b_planes, 2 * n * k_pad, EB, keys, h->num_sms,
+                                 h->stream, &launches, /*cpx=*/2, transB == OZIMMU_OP_C);
+    if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 1);
+    const bool acontig = transA != OZIMMU_OP_N;
+    e = launch_split(A, acontig ? 2 * lda : lda, acontig, m, K2, k_pad, s, w, /*reverse=*/false,
+                     a_planes, m * k_pad, EA, keys, h->num_sms, h->stream, &launches, /*cpx=*/1,
+                     transA == OZIMMU_OP_C);
+    if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 2);
+    GemmArgs ga{};
+    ga.a_planes = a_planes;
+    ga.b_planes = b_planes;
+    ga.EA = EA;
+    ga.EB = EB;
+    ga.m = m;
+    ga.n = 2 * n;
+    ga.k_pad = k_pad;
+    ga.s = s;
+    ga.w = w;
+    ga.alpha = alpha[0];
+    ga.alpha_im = alpha[1];
+    ga.beta = beta[0];
+    ga.beta_im = beta[1];
+    ga.C = C;
+    ga.ldc = ldc;
+    ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
+    static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
+    ga.wave_counter = no_sync ? nullptr : reinterpret_cast<unsigned int *>(base + L.sync);
+    e = launch_gemm(ga, gp, EPI_ZGEMM, h->stream, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 3);
+    mark_done(h);
+    fill_report(h, s, w, m, n, K2, &gp, launches,
+                (int64_t)s * (m + 2 * n) * k_pad + 4 * (m + 2 * n));
+    h->report.int8_macs = (int64_t)s * (s + 1) / 2 * m * (2 * n) * K2;
     return OZIMMU_SUCCESS;
 }
 

@@ -28,6 +28,7 @@ struct KParams {
     uint32_t tmem_cols;
     int mode;
     double alpha, beta;
+    double alpha_im, beta_im;
     const int32_t *EA, *EB;
     double *C;
     int64_t ldc;
@@ -92,6 +93,59 @@ __device__ __forceinline__ void wave_sync(const KParams &P, int64_t wave) {
     while (ld_acquire(P.wave_counter) < target) {
         if (globaltimer() - t0 > 200000ull) break;  // 200 us cap
         __nanosleep(256);
+    }
+}
+
+// X = acc 2^e with ldexp semantics (reading A7): exact power-of-two multiply in range.
+__device__ __forceinline__ double scale_x(double acc, int32_t ea, int32_t eb) {
+    if (ea == kExpNonFinite || eb == kExpNonFinite) return __longlong_as_double(0x7ff8000000000000ll);
+    const int e = ea + eb;
+    if (e >= -1022 && e <= 1023) return __dmul_rn(acc, pow2(e));  // one rounding, 2^e exact
+    return ldexp(acc, e);
+}
+// z = a x for complex a, x (ZGEMM reading A16): re = fma(ar, xr, -(ai xi)), im = fma(ar, xi, ai xr)
+__device__ __forceinline__ void cmul(double ar, double ai, double xr, double xi, double &zr,
+                                     double &zi) {
+    zr = __fma_rn(ar, xr, -__dmul_rn(ai, xi));
+    zi = __fma_rn(ar, xi, __dmul_rn(ai, xr));
+}
+
+// Final output of one row (this thread) of the tile: real C (reading A8) or complex C.
+template <int NC>
+__device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[NC],
+                                          const int32_t *ebt, int32_t ea, int64_t row,
+                                          int64_t nb) {
+    if (P.mode == EPI_DGEMM) {
+        double *crow = P.C + row;
+#pragma unroll
+        for (int i = 0; i < NC; ++i) {
+            const int64_t col = nb * NC + i;
+            if (col >= P.n) break;
+            const double X = scale_x(acc[i], ea, ebt[i]);
+            double *cp = crow + col * P.ldc;
+            *cp = P.beta == 0.0 ? __dmul_rn(P.alpha, X)
+                                : __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
+        }
+    } else {  // EPI_ZGEMM: columns (2j, 2j+1) = (Re, Im) of complex column j
+        const bool beta0 = P.beta == 0.0 && P.beta_im == 0.0;
+#pragma unroll
+        for (int i = 0; i < NC; i += 2) {
+            const int64_t col = nb * NC + i;
+            if (col >= P.n) break;
+            const double xr = scale_x(acc[i], ea, ebt[i]);
+            const double xi = scale_x(acc[i + 1], ea, ebt[i + 1]);
+            double tr, ti;
+            cmul(P.alpha, P.alpha_im, xr, xi, tr, ti);
+            double2 *cp = reinterpret_cast<double2 *>(P.C) + row + (col >> 1) * P.ldc;
+            if (!beta0) {
+                const double2 c = *cp;
+                double ur, ui;
+                cmul(P.beta, P.beta_im, c.x, c.y, ur, ui);
+                tr = __dadd_rn(tr, ur);
+                ti = __dadd_rn(ti, ui);
+            }
+            *cp = make_double2(tr, ti);
+        }
     }
 }
 
@@ -360,10 +414,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tile_coords(t, P, mb, nb);
             const int64_t row = mb * kBlockM + row_local;
             const bool row_ok = row < P.m;
-            const int32_t ea = (P.mode == EPI_DGEMM && row_ok) ? P.EA[row] : 0;
+            const bool fp_out = P.mode == EPI_DGEMM || P.mode == EPI_ZGEMM;
+            const int32_t ea = (fp_out && row_ok) ? P.EA[row] : 0;
             // stage this tile's column exponents in shared memory while the MMAs run
             int32_t *ebt = eb_s[tile_iter & 1];
-            if (P.mode == EPI_DGEMM && row_local < (uint32_t)NC) {
+            if (fp_out && row_local < (uint32_t)NC) {
                 const int64_t col = nb * NC + row_local;
                 ebt[row_local] = col < P.n ? P.EB[col] : 0;
             }
@@ -374,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 long long ce = P.stats ? clock64() : 0;
                 const bool first = c == 0, last = c == P.k_chunks - 1;
-                if (P.mode == EPI_DGEMM && !scr) {
+                if (fp_out && !scr) {
                     // ---------------- fast path: one period, FP64 result ----------------
                     double acc[NC];
 #pragma unroll
@@ -421,26 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_arrive(tmem_empty);  // accumulator free: next period may start
                     if (P.stats) st_et += clock64() - ce;
                     long long cs0 = P.stats ? clock64() : 0;
-                    if (row_ok) {
-                        double *crow = P.C + row;
-#pragma unroll
-                        for (int i = 0; i < NC; ++i) {
-                            const int64_t col = nb * NC + i;
-                            if (col >= P.n) break;
-                            const int32_t eb = ebt[i];
-                            const int e = ea + eb;
-                            double X;
-                            if (ea == kExpNonFinite || eb == kExpNonFinite)
-                                X = __longlong_as_double(0x7ff8000000000000ll);
-                            else if (e >= -1022 && e <= 1023)
-                                X = __dmul_rn(acc[i], pow2(e));  // = ldexp: one rounding
-                            else
-                                X = ldexp(acc[i], e);
-                            double *cp = crow + col * P.ldc;
-                            *cp = P.beta == 0.0 ? __dmul_rn(P.alpha, X)
-                                                : __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
-                        }
-                    }
+                    if (row_ok) store_row<NC>(P, acc, ebt, ea, row, nb);
                     if (P.stats) {
                         st_es += clock64() - cs0;
                         st_e += clock64() - ce;
@@ -483,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     continue;
                                 }
                             }
-                            if (P.mode == EPI_DGEMM) {
+                            if (fp_out) {
                                 acc[i] = __fma_rn((double)Lg, sc, acc[i]);
                             } else if (row_ok) {
                                 const int64_t col = nb * NC + i;
@@ -500,25 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(tmem_empty);
-                if (last && P.mode == EPI_DGEMM && row_ok) {
-#pragma unroll
-                    for (int i = 0; i < NC; ++i) {
-                        const int64_t col = nb * NC + i;
-                        if (col >= P.n) break;
-                        const int32_t eb = ebt[i];
-                        const int e = ea + eb;
-                        double X;
-                        if (ea == kExpNonFinite || eb == kExpNonFinite)
-                            X = __longlong_as_double(0x7ff8000000000000ll);
-                        else if (e >= -1022 && e <= 1023)
-                            X = __dmul_rn(acc[i], pow2(e));
-                        else
-                            X = ldexp(acc[i], e);
-                        double *cp = P.C + row + col * P.ldc;
-                        *cp = P.beta == 0.0 ? __dmul_rn(P.alpha, X)
-                                            : __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
-                    }
-                }
+                if (last && fp_out && row_ok) store_row<NC>(P, acc, ebt, ea, row, nb);
                 if (P.stats) st_e += clock64() - ce;
             }
         }
@@ -603,6 +621,8 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.mode = mode;
     P.alpha = a.alpha;
     P.beta = a.beta;
+    P.alpha_im = a.alpha_im;
+    P.beta_im = a.beta_im;
     P.EA = a.EA;
     P.EB = a.EB;
     P.C = a.C;

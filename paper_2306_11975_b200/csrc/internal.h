@@ -29,13 +29,18 @@ inline int slice_width(int64_t k) {
 // E[r]: frexp exponent of the vector's max |x| (0 for an all-zero vector,
 // kExpNonFinite if any element is NaN/Inf -- its digits are then all 0).
 // key_scratch: int32[rows] device scratch (strided case only).
+// Complex operands (ZGEMM, reading A16): cpx = 1 -> vectors are complex rows of op(A)
+// (kdim / k_pad count doubles: 2 per element, Im negated if conj); cpx = 2 -> vectors are
+// complex columns of op(B), each emitting two plane rows 2r = (Re, -Im, ..) and
+// 2r+1 = (Im, Re, ..).  For strided complex vectors `ld` is in complex elements; for
+// contiguous ones it is in doubles.
 cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
                          int64_t k_pad, int s, int w, bool reverse, int8_t *planes,
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
-                         cudaStream_t st, int *launches);
+                         cudaStream_t st, int *launches, int cpx = 0, int conj = 0);
 
 // ---- fused GEMM (A4 + A5) ----------------------------------------------------------------
-enum EpiMode : int { EPI_DGEMM = 0, EPI_LEVELS_I64 = 1, EPI_PAIR_I32 = 2 };
+enum EpiMode : int { EPI_DGEMM = 0, EPI_LEVELS_I64 = 1, EPI_PAIR_I32 = 2, EPI_ZGEMM = 3 };
 
 struct GemmArgs {
     const int8_t *a_planes;  // [s][m][k_pad], natural slice order
@@ -44,7 +49,9 @@ struct GemmArgs {
     int64_t m, n, k_pad;
     int s, w;
     double alpha, beta;
-    double *C;               // EPI_DGEMM: column-major, ldc
+    double alpha_im, beta_im;  // EPI_ZGEMM: complex alpha / beta
+    double *C;               // EPI_DGEMM: column-major, ldc; EPI_ZGEMM: interleaved complex,
+                             // ldc in complex elements, GEMM columns 2j / 2j+1 = Re / Im of C(:,j)
     int64_t ldc;
     void *out;               // EPI_LEVELS_I64: int64 [s][n][m];  EPI_PAIR_I32: int32 [n][m]
     int64_t *chunk_scratch;  // per-CTA partial level sums when k_chunks > 1

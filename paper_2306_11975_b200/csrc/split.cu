@@ -103,6 +103,42 @@ __device__ __forceinline__ void store_digits(const Digits<W, S> (&dg)[8], int s,
     }
 }
 
+// Output of one 8-element chunk (elements l0..l0+7 of input vector r) for the three
+// operand forms (ZGEMM reading A16, real embedding with interleaved K):
+//   CPX 0  real vector                    -> row r
+//   CPX 1  complex row of op(A) (re, im)   -> row r, Im negated if conj
+//   CPX 2  complex column of op(B)         -> row 2r   = (Re, -Im, ...)
+//                                             row 2r+1 = (Im,  Re, ...)   (Im := -Im if conj)
+// Sign changes and the (re, im) swap act on the digits (sign-magnitude: digits of -x are
+// the negated digits of x), so each input element is digitised once.
+template <int W, int S, int CPX>
+__device__ __forceinline__ void emit(Digits<W, S> (&dg)[8], int s, int reverse, int conj,
+                                     int8_t *planes, int64_t r, int64_t l0, int64_t k_pad,
+                                     int64_t plane_stride) {
+    if constexpr (CPX == 0) {
+        store_digits<W, S>(dg, s, reverse, planes + r * k_pad + l0, plane_stride);
+    } else if constexpr (CPX == 1) {
+        if (conj) {
+#pragma unroll
+            for (int i = 1; i < 8; i += 2) dg[i].sm = ~dg[i].sm;
+        }
+        store_digits<W, S>(dg, s, reverse, planes + r * k_pad + l0, plane_stride);
+    } else {
+        Digits<W, S> sw[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            sw[i] = dg[i ^ 1];
+            if (conj && (i & 1) == 0) sw[i].sm = ~sw[i].sm;  // Im of a conjugated element
+        }
+        if (!conj) {
+#pragma unroll
+            for (int i = 1; i < 8; i += 2) dg[i].sm = ~dg[i].sm;  // -Im
+        }
+        store_digits<W, S>(dg, s, reverse, planes + (2 * r) * k_pad + l0, plane_stride);
+        store_digits<W, S>(sw, s, reverse, planes + (2 * r + 1) * k_pad + l0, plane_stride);
+    }
+}
+
 __device__ __forceinline__ void load8(const double *v, int64_t l0, int64_t kdim, bool al16,
                                       double (&x)[8]) {
     if (al16 && l0 + 8 <= kdim) {
@@ -124,10 +160,10 @@ __device__ __forceinline__ void load8(const double *v, int64_t l0, int64_t kdim,
 // TPR threads per vector, one pass for the exponent (max reduction), one pass for
 // the digits (the second read of a <= 128 KB row hits L2).
 // ---------------------------------------------------------------------------------
-template <int TPR, int W, int S>
+template <int TPR, int W, int S, int CPX>
 __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__ M, int64_t ld,
                                                       int64_t rows, int64_t kdim, int64_t k_pad,
-                                                      int s, int reverse,
+                                                      int s, int reverse, int conj,
                                                       int8_t *__restrict__ planes,
                                                       int64_t plane_stride, int32_t *__restrict__ E) {
     constexpr int VPB = 256 / TPR;  // vectors per block
@@ -161,7 +197,14 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
     }
     if (!active) return;
     const int32_t Ev = key_to_exp(key);
-    if (t == 0) E[r] = Ev;
+    if (t == 0) {
+        if (CPX == 2) {
+            E[2 * r] = Ev;
+            E[2 * r + 1] = Ev;
+        } else {
+            E[r] = Ev;
+        }
+    }
     const bool bad = Ev == kExpNonFinite;
 
     // ---- pass 2: digits ----
@@ -172,7 +215,7 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
         Digits<W, S> dg[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-        store_digits<W, S>(dg, s, reverse, planes + r * k_pad + l0, plane_stride);
+        emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
     }
 }
 
@@ -182,6 +225,7 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
 // ---------------------------------------------------------------------------------
 
 // Pass 1: one thread per vector, a slice of l per blockIdx.y; atomicMax of the key.
+template <int CPX>
 __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restrict__ M, int64_t ld,
                                                          int64_t rows, int64_t kdim, int64_t lchunk,
                                                          int32_t *__restrict__ keys) {
@@ -191,6 +235,21 @@ __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restric
     const int64_t l1 = min(kdim, l0 + lchunk);
     int32_t key = kKeyEmpty;
     int64_t l = l0;
+    if constexpr (CPX != 0) {  // kdim counts complex elements here; (re, im) pairs: 16-byte loads
+        const double2 *Mc = reinterpret_cast<const double2 *>(M);
+        for (; l + 4 <= l1; l += 4) {
+            double2 x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(Mc + r + (l + i) * ld);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) key = max(key, max(exp_key(x[i].x), exp_key(x[i].y)));
+        }
+        for (; l < l1; ++l) {
+            const double2 x = __ldg(Mc + r + l * ld);
+            key = max(key, max(exp_key(x.x), exp_key(x.y)));
+        }
+        if (key != kKeyEmpty) atomicMax(keys + r, key);
+    } else {
     for (; l + 8 <= l1; l += 8) {
         double x[8];
 #pragma unroll
@@ -200,6 +259,7 @@ __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restric
     }
     for (; l < l1; ++l) key = max(key, exp_key(__ldg(M + r + l * ld)));
     if (key != kKeyEmpty) atomicMax(keys + r, key);
+    }
 }
 
 // Pass 2: 32 vectors x 128 elements per block, transposed through shared memory so that
@@ -212,10 +272,10 @@ __device__ __forceinline__ int tslot(int r, int l) {
     return 2 * (q ^ ((q >> 2) & 7) ^ (r & 7)) + (l & 1);
 }
 
-template <int W, int S>
+template <int W, int S, int CPX>
 __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict__ M, int64_t ld,
                                                        int64_t rows, int64_t kdim, int64_t k_pad,
-                                                       int s, int reverse,
+                                                       int s, int reverse, int conj,
                                                        const int32_t *__restrict__ keys,
                                                        int8_t *__restrict__ planes,
                                                        int64_t plane_stride,
@@ -230,7 +290,14 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
         int32_t e = 0;
         if (r < rows) {
             e = key_to_exp(keys[r]);
-            if (blockIdx.y == 0) E[r] = e;
+            if (blockIdx.y == 0) {
+                if (CPX == 2) {
+                    E[2 * r] = e;
+                    E[2 * r + 1] = e;
+                } else {
+                    E[r] = e;
+                }
+            }
         }
         exps[tid] = e;
     }
@@ -238,11 +305,26 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
     {
         const int rr = tid & 31;
         const int64_t r = r0 + rr;
+        if (CPX) {
+            // kdim counts doubles (2 per complex element); complex element (r, lc) is the
+            // 16-byte pair at 2 (r + lc ld)
+            const double2 *Mc = reinterpret_cast<const double2 *>(M);
 #pragma unroll 4
-        for (int it = 0; it < 16; ++it) {
-            const int ll = (tid >> 5) + 8 * it;
-            const int64_t l = l0 + ll;
-            tile[rr][tslot(rr, ll)] = (r < rows && l < kdim) ? __ldg(M + r + l * ld) : 0.0;
+            for (int it = 0; it < 8; ++it) {
+                const int lc = (tid >> 5) + 8 * it;  // 0..63
+                const int64_t l = l0 + 2 * lc;
+                double2 x = make_double2(0.0, 0.0);
+                if (r < rows && l < kdim) x = __ldg(Mc + r + (l >> 1) * ld);
+                tile[rr][tslot(rr, 2 * lc)] = x.x;
+                tile[rr][tslot(rr, 2 * lc + 1)] = x.y;
+            }
+        } else {
+#pragma unroll 4
+            for (int it = 0; it < 16; ++it) {
+                const int ll = (tid >> 5) + 8 * it;
+                const int64_t l = l0 + ll;
+                tile[rr][tslot(rr, ll)] = (r < rows && l < kdim) ? __ldg(M + r + l * ld) : 0.0;
+            }
         }
     }
     __syncthreads();
@@ -265,22 +347,23 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
         Digits<W, S> dg[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-        store_digits<W, S>(dg, s, reverse, planes + r * k_pad + lb, plane_stride);
+        emit<W, S, CPX>(dg, s, reverse, conj, planes, r, lb, k_pad, plane_stride);
     }
 }
 
-template <int W, int S>
+template <int W, int S, int CPX>
 cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t rows,
-                           int64_t kdim, int64_t k_pad, int s, bool reverse, int8_t *planes,
-                           int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
-                           cudaStream_t st, int *launches) {
+                           int64_t kdim, int64_t k_pad, int s, bool reverse, int conj,
+                           int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
+                           int num_sms, cudaStream_t st, int *launches) {
+    // kdim / k_pad count doubles of the (embedded) vector: 2 per complex element
     if (contiguous) {
         if (k_pad >= 2048) {
-            k_split_contig<256, W, S><<<(unsigned)rows, 256, 0, st>>>(
-                M, ld, rows, kdim, k_pad, s, reverse, planes, plane_stride, E);
+            k_split_contig<256, W, S, CPX><<<(unsigned)rows, 256, 0, st>>>(
+                M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E);
         } else {
-            k_split_contig<32, W, S><<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(
-                M, ld, rows, kdim, k_pad, s, reverse, planes, plane_stride, E);
+            k_split_contig<32, W, S, CPX><<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(
+                M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E);
         }
         ++*launches;
         return cudaGetLastError();
@@ -288,37 +371,60 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
     // strided: exponent scan then transposing slice
     cudaError_t e = cudaMemsetAsync(key_scratch, 0x80, sizeof(int32_t) * rows, st);
     if (e != cudaSuccess) return e;
+    const int64_t kel = CPX ? kdim / 2 : kdim;  // elements along the vector
     const int64_t rblocks = ceil_div(rows, 256);
     int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
     ysplit = ysplit < 1 ? 1 : ysplit;
-    int64_t lchunk = round_up(ceil_div(kdim, ysplit), 8);
+    int64_t lchunk = round_up(ceil_div(kel, ysplit), 8);
     if (lchunk < 64) lchunk = 64;
-    ysplit = ceil_div(kdim, lchunk);
+    ysplit = ceil_div(kel, lchunk);
     if (ysplit < 1) ysplit = 1;
-    k_expscan_strided<<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-        M, ld, rows, kdim, lchunk, key_scratch);
+    k_expscan_strided<CPX ? 1 : 0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+        M, ld, rows, kel, lchunk, key_scratch);
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_split_strided<W, S><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(k_pad, 128)), 256,
-                            0, st>>>(M, ld, rows, kdim, k_pad, s, reverse, key_scratch, planes,
-                                     plane_stride, E);
+    k_split_strided<W, S, CPX><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(k_pad, 128)),
+                                 256, 0, st>>>(M, ld, rows, kdim, k_pad, s, reverse, conj,
+                                               key_scratch, planes, plane_stride, E);
     ++*launches;
     return cudaGetLastError();
 }
 
-template <int W>
+template <int W, int CPX>
 cudaError_t launch_split_w(const double *M, int64_t ld, bool contiguous, int64_t rows,
-                           int64_t kdim, int64_t k_pad, int s, bool reverse, int8_t *planes,
-                           int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
-                           cudaStream_t st, int *launches) {
+                           int64_t kdim, int64_t k_pad, int s, bool reverse, int conj,
+                           int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
+                           int num_sms, cudaStream_t st, int *launches) {
     if (s <= 9)
-        return launch_split_t<W, 9>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
-                                    plane_stride, E, key_scratch, num_sms, st, launches);
+        return launch_split_t<W, 9, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                         planes, plane_stride, E, key_scratch, num_sms, st,
+                                         launches);
     if (s <= 16)
-        return launch_split_t<W, 16>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
-                                     plane_stride, E, key_scratch, num_sms, st, launches);
-    return launch_split_t<W, 32>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
-                                 plane_stride, E, key_scratch, num_sms, st, launches);
+        return launch_split_t<W, 16, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                          planes, plane_stride, E, key_scratch, num_sms, st,
+                                          launches);
+    return launch_split_t<W, 32, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                      planes, plane_stride, E, key_scratch, num_sms, st,
+                                      launches);
+}
+
+template <int CPX>
+cudaError_t launch_split_c(const double *M, int64_t ld, bool contiguous, int64_t rows,
+                           int64_t kdim, int64_t k_pad, int s, int w, bool reverse, int conj,
+                           int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
+                           int num_sms, cudaStream_t st, int *launches) {
+    switch (w) {
+    case 7: return launch_split_w<7, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                          planes, plane_stride, E, key_scratch, num_sms, st,
+                                          launches);
+    case 6: return launch_split_w<6, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                          planes, plane_stride, E, key_scratch, num_sms, st,
+                                          launches);
+    case 5: return launch_split_w<5, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                          planes, plane_stride, E, key_scratch, num_sms, st,
+                                          launches);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace
@@ -326,16 +432,16 @@ cudaError_t launch_split_w(const double *M, int64_t ld, bool contiguous, int64_t
 cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
                          int64_t k_pad, int s, int w, bool reverse, int8_t *planes,
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
-                         cudaStream_t st, int *launches) {
+                         cudaStream_t st, int *launches, int cpx, int conj) {
     if (rows <= 0) return cudaSuccess;
     if (s < 1 || s > 32) return cudaErrorInvalidValue;
-    switch (w) {
-    case 7: return launch_split_w<7>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
-                                     plane_stride, E, key_scratch, num_sms, st, launches);
-    case 6: return launch_split_w<6>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
-                                     plane_stride, E, key_scratch, num_sms, st, launches);
-    case 5: return launch_split_w<5>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, planes,
-                                     plane_stride, E, key_scratch, num_sms, st, launches);
+    switch (cpx) {
+    case 0: return launch_split_c<0>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, 0,
+                                     planes, plane_stride, E, key_scratch, num_sms, st, launches);
+    case 1: return launch_split_c<1>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, conj,
+                                     planes, plane_stride, E, key_scratch, num_sms, st, launches);
+    case 2: return launch_split_c<2>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, conj,
+                                     planes, plane_stride, E, key_scratch, num_sms, st, launches);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -26,7 +26,7 @@ EXPORTS = [
     "ozimmu_set_workspace", "ozimmu_get_report", "ozimmu_version", "ozimmu_status_string",
     "ozimmu_dgemm", "ozimmu_b_slices_bytes", "ozimmu_slice_b", "ozimmu_dgemm_presliced_b",
     "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
-    "ozimmu_timing_enable", "ozimmu_timing_read",
+    "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
 ]
 
 
@@ -82,6 +82,8 @@ def lib():
         "ozimmu_debug_level_sums": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, i32, vp], i32),
         "ozimmu_debug_pair": ([H, vp, vp, i64, i64, i64, vp], i32),
         "ozimmu_timing_enable": ([H, i32], i32),
+        "ozimmu_zgemm": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32], i32),
+        "ozimmu_zgemm_workspace_bytes": ([i32, i32, i64, i64, i64, i32], sz),
         "ozimmu_timing_read": ([H, ct.POINTER(Timing), i32], i32),
     }
     for name, (args, res) in sig.items():
@@ -180,6 +182,15 @@ class Handle:
         _check("ozimmu_dgemm", lib().ozimmu_dgemm(
             self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _ptr(A), lda, _ptr(B), ldb,
             _d(beta), _ptr(C), ldc, int(num_slices)))
+
+    def zgemm(self, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_slices):
+        """Complex GEMM: A, B, C interleaved complex (e.g. torch.complex128), ld in complex
+        elements, alpha / beta Python complex numbers."""
+        a = (ct.c_double * 2)(complex(alpha).real, complex(alpha).imag)
+        b = (ct.c_double * 2)(complex(beta).real, complex(beta).imag)
+        _check("ozimmu_zgemm", lib().ozimmu_zgemm(
+            self._h, OP[transA], OP[transB], m, n, k, a, _ptr(A), lda, _ptr(B), ldb, b, _ptr(C),
+            ldc, int(num_slices)))
 
     def slice_b(self, transB, k, n, B, ldb, num_slices, b_slices):
         _check("ozimmu_slice_b", lib().ozimmu_slice_b(
