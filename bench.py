@@ -31,6 +31,12 @@ WORKLOADS = {
                     "GPUs + NCCL broadcast of B's INT8 slices"),
     "C3": dict(m=8192, n=8192, k=8192, phi=0.5, s=9, seeds=(301, 302),
                desc="C3: DGEMM m=n=k=8192, phi=0.5, s=9 (FP64-equivalent)"),
+    # ZGEMM of BASELINE config 5: one d-qubit gate on an N-qubit state vector,
+    # matmul-(2^(N-d), 2^d, 2^d), N = 28, d = 12, s = 12 (the T = 0 AUTO choice
+    # for the paper's circuits was INT8x12/13)
+    "C5": dict(m=2 ** 16, n=2 ** 12, k=2 ** 12, phi=0.1, s=12, seeds=(501, 502), complex=True,
+               desc="C5: ZGEMM matmul-(2^16, 2^12, 2^12) = one 12-qubit Haar gate on a 28-qubit "
+                    "state vector, s=12"),
 }
 METRIC = "effective DGEMM TFLOP/s (2mnk/t) vs cuBLAS DGEMM at 1/2/4/8 B200; max rel err"
 INT8_PEAK_NOTE = ("INT8 dense peak = 2 x measured bf16 cuBLAS (nominal 4.5/2.25 POPS ratio); "
@@ -145,6 +151,10 @@ def run_reference(args, wl):
     rank = env_int("RANK", 0)
     if rank != 0:
         return
+    if wl.get("complex"):
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm times the real "
+                          "workloads (C3/C4); C5 is measured GPU-only"}), flush=True)
+        return
     import oracle as O
     cores = os.cpu_count()
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
@@ -189,6 +199,80 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def run_zgemm(args, wl):
+    """Single-GPU ZGEMM throughput (8mnk/t) vs cuBLAS ZGEMM on the config-5 shape."""
+    import torch
+
+    import paper_2306_11975_b200 as oz
+    m, n, k, s = wl["m"], wl["n"], wl["k"], wl["s"]
+    torch.cuda.set_device(0)
+    psi = synth.gen_phi_complex(m, k, wl["phi"], wl["seeds"][0])
+    psi /= np.linalg.norm(psi)
+    U = synth.haar_unitary(k, wl["seeds"][1])
+    dA = torch.from_numpy(np.ascontiguousarray(psi.ravel(order="F"))).cuda()
+    dB = torch.from_numpy(np.ascontiguousarray(U.ravel(order="F"))).cuda()
+    dC = torch.empty(m * n, dtype=torch.complex128, device="cuda")
+    h = oz.Handle(0)
+    stream = torch.cuda.current_stream()
+    h.set_stream(stream)
+
+    def step():
+        h.zgemm("N", "T", m, n, k, 1.0, dA, m, dB, n, 0.0, dC, m, s)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rep = h.report()
+    h.timing_enable(args.steps + 1)
+    clocks = ClockSampler(0)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    phases = h.timing_read(args.steps + 1)
+    flops = 8.0 * m * n * k
+    value = flops / (ms / 1e3) / 1e12
+    gemm_ms = float(np.mean([p["gemm_ms"] for p in phases]))
+    peaks, src = load_peaks()
+    int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    ops = float(s * (s + 1)) * m * (2 * n) * (2 * k)
+    achieved = ops / (gemm_ms / 1e3) / 1e12
+    Am = dA.view(k, m).t()
+    Bm = dB.view(k, n)  # U stored column-major = U^T row-major; op(B) = U^T
+    Cm = torch.empty(m, n, dtype=torch.complex128, device="cuda")
+    for _ in range(2):
+        torch.matmul(Am, Bm, out=Cm)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(max(3, args.steps // 2)):
+        torch.matmul(Am, Bm, out=Cm)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    cms = e0.elapsed_time(e1) / max(3, args.steps // 2)
+    cv = flops / (cms / 1e3) / 1e12
+    line = {"metric": "effective ZGEMM TFLOP/s (8mnk/t) vs cuBLAS ZGEMM", "value": value,
+            "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "i8", "data": "synthetic",
+            "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s,
+                       "parallelism": "single GPU", "l2": "inputs larger than L2",
+                       "plan": {kk: rep[kk] for kk in ("tile_n", "k_block", "stages",
+                                                      "k_chunks", "acc_regions")}},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": int8_peak,
+                         "unit": "TFLOP/s", "frac": achieved / int8_peak, "traffic": None,
+                         "gemm_ms": gemm_ms, "peak_source": src},
+            "cublas_zgemm": {"value": cv, "unit": "TFLOP/s", "ms_per_step": cms,
+                             "speedup_ozimmu_vs_cublas": value / cv},
+            "clocks": clk, "gpu_launches": rep["launches"] * args.steps}
+    print(json.dumps(line), flush=True)
+    h.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -208,6 +292,9 @@ def main():
         wl["s"] = args.slices
     if args.impl == "reference":
         run_reference(args, wl)
+        return
+    if wl.get("complex"):
+        run_zgemm(args, wl)
         return
 
     import torch
