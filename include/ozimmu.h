@@ -37,8 +37,9 @@
  *  - Quick returns (BLAS): m == 0 or n == 0 -> no-op; alpha == 0 or k == 0 ->
  *    C = beta*C without reading A or B; beta == 0 -> C is not read (NaN in C is
  *    ignored).
- *  - num_slices = s in [1, OZIMMU_MAX_SLICES].  0 (the paper's INT8-AUTO,
- *    P:656-659) is reserved and returns OZIMMU_ERR_UNSUPPORTED.
+ *  - num_slices = s in [1, OZIMMU_MAX_SLICES], or 0 = INT8-AUTO: s is chosen
+ *    per call from the inputs (ozimmu_set_auto); an AUTO call synchronises its stream once
+ *    to read the mantissa-loss statistics (the paper's "check all the elements" pass).
  *  - k is limited to OZIMMU_MAX_K (w >= 5); larger k returns OZIMMU_ERR_UNSUPPORTED.
  *  - Non-finite inputs (reading A9): if row i of op(A) or column j of op(B)
  *    contains NaN/Inf, C(i,j) = NaN (for alpha != 0).  No error is returned.
@@ -158,6 +159,21 @@ OZIMMU_API ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, o
 /* Workspace bytes for ozimmu_zgemm (0 on invalid input). */
 OZIMMU_API size_t ozimmu_zgemm_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
                                     int64_t n, int64_t k, int num_slices);
+
+/* INT8-AUTO (NEXT row f2; "we select the number of splits so that the average
+ * mantissa loss in the splitting process is equal to or smaller than a threshold T").
+ * Reading A17: for a nonzero finite x of a row of op(A) / column of op(B) with exponent E,
+ * the significant bits of |x|/2^E occupy positions lead = E - ilogb(x) .. t_last =
+ * lead + vlen - 1 (vlen: bits from the MSB to the last 1 of the significand);
+ * loss_s(x) = min(vlen, max(0, t_last - s*w)); s = the smallest s in [1, s_max] whose mean
+ * loss over the nonzero finite elements is <= T for both operands (s_max if none).
+ * ozimmu_set_auto sets T (>= 0, default 0) and s_max (default 20) for num_slices = 0 calls;
+ * ozimmu_auto_splits returns the s such a call would use (synchronises the stream). */
+OZIMMU_API ozimmu_status_t ozimmu_set_auto(ozimmu_handle_t h, double threshold, int s_max);
+OZIMMU_API ozimmu_status_t ozimmu_auto_splits(ozimmu_handle_t h, ozimmu_op_t transA,
+                                   ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                   const double *A, int64_t lda, const double *B, int64_t ldb,
+                                   int *num_slices_out);
 
 /* ---- split-phase entry points (multi-GPU: slice B once, broadcast, reuse) -----
  * A "B-slice buffer" is one contiguous device buffer holding the INT8 planes of

@@ -48,6 +48,10 @@ def lib():
         L.dd_zgemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
                                    vp, vp, vp, vp]
         L.dd_zgemm_sub.restype = i32
+        L.oz_ref_mantissa_loss.argtypes = [i32, i64, i64, vp, i64, i32, i32, vp, vp]
+        L.oz_ref_mantissa_loss.restype = i32
+        L.oz_ref_auto_splits.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, dbl, i32]
+        L.oz_ref_auto_splits.restype = i32
         L.dd_two_sum.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
         L.dd_two_prod.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
         L.dd_gemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
@@ -190,6 +194,29 @@ def level_sums(transA, transB, m, n, k, A, lda, B, ldb, s, rows=None, cols=None)
     if rc:
         raise ValueError(f"oz_ref_level_sums_sub failed rc={rc}")
     return out
+
+
+def mantissa_loss(M, trans, rows, kdim, ld, w, s_max):
+    """f2 (reading A17): (loss_sum[s-1] for s = 1..s_max, nnz) over the vectors of op(M)."""
+    M = _f64(M)
+    ls = np.zeros(s_max, dtype=np.int64)
+    nnz = np.zeros(1, dtype=np.int64)
+    rc = lib().oz_ref_mantissa_loss(int(trans), rows, kdim, _p(M), int(ld), int(w), int(s_max),
+                                    _p(ls), _p(nnz))
+    if rc:
+        raise ValueError("oz_ref_mantissa_loss failed")
+    return ls, int(nnz[0])
+
+
+def auto_splits(transA, transB, m, n, k, A, lda, B, ldb, T, s_max=32):
+    """f2 INT8-AUTO: smallest s with both mean mantissa losses <= T."""
+    A = _f64(A)
+    B = _f64(B)
+    s = lib().oz_ref_auto_splits(OP[transA], OP[transB], m, n, k, _p(A), lda, _p(B), ldb,
+                                 float(T), int(s_max))
+    if s < 0:
+        raise ValueError("oz_ref_auto_splits failed")
+    return s
 
 
 def _c128(a):

@@ -424,3 +424,81 @@ int oz_ref_zgemm_sub(int transA, int transB, int64_t m, int64_t n, int64_t k,
     free(Ah); free(Bh); free(Xh); free(rr); free(cc);
     return err;
 }
+
+/* ------------------------------------------------------------------------- */
+/* f2: INT8-AUTO split selection ("we select the number of splits   */
+/* so that the average mantissa loss in the splitting process is equal to or  */
+/* smaller than a threshold T"; Discussion P:713-734).  Reading A17:          */
+/* for a nonzero finite element x of a vector with exponent E, write          */
+/* |x| / 2^E = sum_t b_t 2^-t; its significant bits occupy positions          */
+/* lead = E - ilogb(x) ... t_last = lead + vlen - 1, vlen = number of bits    */
+/* from the MSB to the last 1 of the significand ("valid mantissa   */
+/* length").  The s digits keep positions 1..s*w, so the bits lost are        */
+/*     loss_s(x) = min(vlen, max(0, t_last - s*w)).                           */
+/* mean_loss(M, s) = mean over the nonzero finite elements of M (0 if none). */
+/* ------------------------------------------------------------------------- */
+
+static int valid_len(double x) /* bits from MSB to last 1 of |x|'s significand */
+{
+    int e;
+    double f = frexp(fabs(x), &e); /* f in [0.5, 1) */
+    int v = 0;
+    while (f != floor(f)) { f = f * 2.0; v++; }
+    return v;
+}
+
+/* Sum of loss_s over the vectors of op(M) as in oz_ref_split (trans, rows, kdim, ld),
+ * for s = 1..s_max (loss_sum[s-1]); nnz = number of nonzero finite elements. */
+int oz_ref_mantissa_loss(int trans, int64_t rows, int64_t kdim, const double *M, int64_t ld,
+                         int w, int s_max, int64_t *loss_sum, int64_t *nnz)
+{
+    if (rows < 0 || kdim < 0 || s_max < 1 || w < 1) return OZR_ERR_ARG;
+    for (int s = 0; s < s_max; ++s) loss_sum[s] = 0;
+    *nnz = 0;
+    for (int64_t r = 0; r < rows; ++r) {
+        double vmax = 0.0;
+        int bad = 0;
+        for (int64_t l = 0; l < kdim; ++l) {
+            double v = trans == 0 ? M[r + l * ld] : M[l + r * ld];
+            if (!isfinite(v)) bad = 1;
+            else if (fabs(v) > vmax) vmax = fabs(v);
+        }
+        if (bad || vmax == 0.0) continue;
+        int E;
+        (void)frexp(vmax, &E);
+        for (int64_t l = 0; l < kdim; ++l) {
+            double v = trans == 0 ? M[r + l * ld] : M[l + r * ld];
+            if (v == 0.0) continue;
+            int lead = E - ilogb(v);
+            int vlen = valid_len(v);
+            int t_last = lead + vlen - 1;
+            *nnz += 1;
+            for (int s = 1; s <= s_max; ++s) {
+                int over = t_last - s * w;
+                int loss = over < 0 ? 0 : (over > vlen ? vlen : over);
+                loss_sum[s - 1] += loss;
+            }
+        }
+    }
+    return OZR_OK;
+}
+
+/* Smallest s in [1, s_max] with mean_loss(op(A) rows, s) <= T and mean_loss(op(B)
+ * columns, s) <= T (mean = (double)loss_sum / (double)nnz, 0 if nnz = 0); s_max if none.
+ * w is the method's slice width for this k (A1). */
+int oz_ref_auto_splits(int transA, int transB, int64_t m, int64_t n, int64_t k,
+                       const double *A, int64_t lda, const double *B, int64_t ldb, double T,
+                       int s_max)
+{
+    if (k < 1 || s_max < 1 || s_max > 64) return -1;
+    int w = oz_ref_slice_width(k);
+    int64_t la[64], lb[64], na = 0, nb = 0;
+    if (oz_ref_mantissa_loss(transA == 0 ? 0 : 1, m, k, A, lda, w, s_max, la, &na)) return -1;
+    if (oz_ref_mantissa_loss(transB == 0 ? 1 : 0, n, k, B, ldb, w, s_max, lb, &nb)) return -1;
+    for (int s = 1; s <= s_max; ++s) {
+        double ma = na ? (double)la[s - 1] / (double)na : 0.0;
+        double mb = nb ? (double)lb[s - 1] / (double)nb : 0.0;
+        if (ma <= T && mb <= T) return s;
+    }
+    return s_max;
+}

@@ -24,6 +24,11 @@ struct ozimmu_ctx {
     cudaEvent_t *events = nullptr;
     int timing_cap = 0;
     int timing_count = 0;
+    // INT8-AUTO (num_slices = 0): threshold T on the mean mantissa loss, s cap
+    double auto_T = 0.0;
+    int auto_smax = 20;
+    int auto_last_s = 0;
+    unsigned long long *auto_dev = nullptr;  // device [2][33] loss sums
 };
 
 namespace {
@@ -143,8 +148,7 @@ ozimmu_status_t check_common(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, i
     if (ldc < (m > 1 ? m : 1)) return OZIMMU_ERR_INVALID_VALUE;
     if (m > 0 && n > 0 && !C) return OZIMMU_ERR_INVALID_VALUE;
     if (m > 0 && k > 0 && *alpha != 0.0 && !A) return OZIMMU_ERR_INVALID_VALUE;
-    if (s == 0) return OZIMMU_ERR_UNSUPPORTED;  // INT8-AUTO not implemented
-    if (s < 0 || s > OZIMMU_MAX_SLICES) return OZIMMU_ERR_INVALID_VALUE;
+    if (s < 0 || s > OZIMMU_MAX_SLICES) return OZIMMU_ERR_INVALID_VALUE;  // 0 = INT8-AUTO
     if (k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
     return OZIMMU_SUCCESS;
 }
@@ -198,6 +202,52 @@ cudaError_t slice_b(ozimmu_handle_t h, ozimmu_op_t transB, int64_t k, int64_t n,
     int32_t *E = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
     return launch_split(B, ldb, contig, n, k, k_pad, s, w, /*reverse=*/true, planes,
                         (int64_t)n * k_pad, E, keys, h->num_sms, h->stream, launches);
+}
+
+// f2 INT8-AUTO (reading A17): exact per-s mantissa-loss sums of the rows of
+// op(A) and the columns of op(B) on the device, one D2H read (the call synchronises the
+// stream), then the smallest s <= s_max whose mean loss is <= T for both operands.
+ozimmu_status_t auto_select(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
+                            int64_t n, int64_t k, const double *A, int64_t lda, const double *B,
+                            int64_t ldb, int *s_out, int *launches, bool cpx = false) {
+    constexpr int NS = 33;
+    const int s_max = h->auto_smax;
+    const int w = slice_width(cpx ? 2 * k : k);
+    if (!h->auto_dev && cudaMalloc(&h->auto_dev, 2 * NS * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return OZIMMU_ERR_WORKSPACE;
+    }
+    void *ws = nullptr;
+    ozimmu_status_t st = get_ws(h, align_up(sizeof(int32_t) * (size_t)(m > n ? m : n)), &ws);
+    if (st) return st;
+    int32_t *keys = static_cast<int32_t *>(ws);
+    cudaError_t e = cudaMemsetAsync(h->auto_dev, 0, 2 * NS * sizeof(unsigned long long), h->stream);
+    const bool ac = transA != OZIMMU_OP_N, bc = transB == OZIMMU_OP_N;
+    // complex: contiguous vectors are 2k doubles (ld in doubles), strided ones k pairs
+    if (e == cudaSuccess)
+        e = launch_mantissa_loss(A, cpx && ac ? 2 * lda : lda, ac, m, cpx && ac ? 2 * k : k, w,
+                                 s_max, h->auto_dev, keys, h->num_sms, h->stream, launches, cpx);
+    if (e == cudaSuccess)
+        e = launch_mantissa_loss(B, cpx && bc ? 2 * ldb : ldb, bc, n, cpx && bc ? 2 * k : k, w,
+                                 s_max, h->auto_dev + NS, keys, h->num_sms, h->stream, launches,
+                                 cpx);
+    unsigned long long host[2 * NS];
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(host, h->auto_dev, sizeof(host), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    int chosen = s_max;
+    for (int s = 1; s <= s_max; ++s) {
+        const double ma = host[32] ? (double)host[s - 1] / (double)host[32] : 0.0;
+        const double mb = host[NS + 32] ? (double)host[NS + s - 1] / (double)host[NS + 32] : 0.0;
+        if (ma <= h->auto_T && mb <= h->auto_T) {
+            chosen = s;
+            break;
+        }
+    }
+    *s_out = chosen;
+    h->auto_last_s = chosen;
+    return OZIMMU_SUCCESS;
 }
 
 ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t n, int64_t k,
@@ -362,8 +412,33 @@ int ozimmu_timing_read(ozimmu_handle_t h, ozimmu_timing_t *out, int max_out) {
     return n;
 }
 
+ozimmu_status_t ozimmu_set_auto(ozimmu_handle_t h, double threshold, int s_max) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!(threshold >= 0.0) || s_max < 1 || s_max > OZIMMU_MAX_SLICES) return OZIMMU_ERR_INVALID_VALUE;
+    h->auto_T = threshold;
+    h->auto_smax = s_max;
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_auto_splits(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB,
+                                   int64_t m, int64_t n, int64_t k, const double *A, int64_t lda,
+                                   const double *B, int64_t ldb, int *num_slices_out) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!num_slices_out || !valid_op(transA) || !valid_op(transB) || m < 0 || n < 0 || k < 1)
+        return OZIMMU_ERR_INVALID_VALUE;
+    if (lda < (transA == OZIMMU_OP_N ? (m > 1 ? m : 1) : k) ||
+        ldb < (transB == OZIMMU_OP_N ? k : (n > 1 ? n : 1)))
+        return OZIMMU_ERR_INVALID_VALUE;
+    if (k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    if ((m > 0 && !A) || (n > 0 && !B)) return OZIMMU_ERR_INVALID_VALUE;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    int launches = 0;
+    return auto_select(h, transA, transB, m, n, k, A, lda, B, ldb, num_slices_out, &launches);
+}
+
 ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
     if (!h) return OZIMMU_SUCCESS;
+    if (h->auto_dev) cudaFree(h->auto_dev);
     if (h->events) {
         cudaStreamSynchronize(h->stream);
         for (int i = 0; i < 4 * h->timing_cap; ++i) cudaEventDestroy(h->events[i]);
@@ -427,8 +502,16 @@ ozimmu_status_t ozimmu_dgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t 
     }
     if (*alpha == 0.0 || k == 0) return scale_only(h, m, n, *beta, C, ldc);
     if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
-    return gemm_core(h, transA, m, n, k, *alpha, A, lda, nullptr, transB, B, ldb, *beta, C, ldc,
-                     num_slices);
+    int auto_launches = 0;
+    if (num_slices == 0) {  // INT8-AUTO
+        ozimmu_status_t st2 = auto_select(h, transA, transB, m, n, k, A, lda, B, ldb, &num_slices,
+                                          &auto_launches);
+        if (st2) return st2;
+    }
+    ozimmu_status_t r = gemm_core(h, transA, m, n, k, *alpha, A, lda, nullptr, transB, B, ldb,
+                                  *beta, C, ldc, num_slices);
+    h->report.launches += auto_launches;
+    return r;
 }
 
 size_t ozimmu_b_slices_bytes(int64_t n, int64_t k, int num_slices) {
@@ -656,6 +739,12 @@ ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t 
         fill_report(h, 0, 0, m, n, 0, nullptr, launches, 0);
         return OZIMMU_SUCCESS;
     }
+    int auto_launches = 0;
+    if (num_slices == 0) {  // INT8-AUTO on the embedded (reading A16) operands
+        st = auto_select(h, transA, transB, m, n, k, A, lda, B, ldb, &num_slices, &auto_launches,
+                         /*cpx=*/true);
+        if (st) return st;
+    }
     const int s = num_slices;
     const int64_t K2 = 2 * k;
     const int w = slice_width(K2);
@@ -713,6 +802,7 @@ ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t 
     fill_report(h, s, w, m, n, K2, &gp, launches,
                 (int64_t)s * (m + 2 * n) * k_pad + 4 * (m + 2 * n));
     h->report.int8_macs = (int64_t)s * (s + 1) / 2 * m * (2 * n) * K2;
+    h->report.launches += auto_launches;
     return OZIMMU_SUCCESS;
 }
 

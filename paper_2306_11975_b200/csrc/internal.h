@@ -39,6 +39,12 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
                          cudaStream_t st, int *launches, int cpx = 0, int conj = 0);
 
+// ---- INT8-AUTO mantissa-loss scan (f2) -------------------------------------------------
+cudaError_t launch_mantissa_loss(const double *M, int64_t ld, bool contiguous, int64_t rows,
+                                 int64_t kdim, int w, int s_max, unsigned long long *out,
+                                 int32_t *key_scratch, int num_sms, cudaStream_t st,
+                                 int *launches, int cpx = 0);
+
 // ---- fused GEMM (A4 + A5) ----------------------------------------------------------------
 enum EpiMode : int { EPI_DGEMM = 0, EPI_LEVELS_I64 = 1, EPI_PAIR_I32 = 2, EPI_ZGEMM = 3 };
 

@@ -27,6 +27,7 @@ EXPORTS = [
     "ozimmu_dgemm", "ozimmu_b_slices_bytes", "ozimmu_slice_b", "ozimmu_dgemm_presliced_b",
     "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
     "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
+    "ozimmu_set_auto", "ozimmu_auto_splits",
 ]
 
 
@@ -84,6 +85,8 @@ def lib():
         "ozimmu_timing_enable": ([H, i32], i32),
         "ozimmu_zgemm": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32], i32),
         "ozimmu_zgemm_workspace_bytes": ([i32, i32, i64, i64, i64, i32], sz),
+        "ozimmu_set_auto": ([H, ct.c_double, i32], i32),
+        "ozimmu_auto_splits": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, ct.POINTER(i32)], i32),
         "ozimmu_timing_read": ([H, ct.POINTER(Timing), i32], i32),
     }
     for name, (args, res) in sig.items():
@@ -182,6 +185,16 @@ class Handle:
         _check("ozimmu_dgemm", lib().ozimmu_dgemm(
             self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _ptr(A), lda, _ptr(B), ldb,
             _d(beta), _ptr(C), ldc, int(num_slices)))
+
+    def set_auto(self, threshold, s_max=20):
+        """INT8-AUTO settings for num_slices = 0 calls."""
+        _check("ozimmu_set_auto", lib().ozimmu_set_auto(self._h, float(threshold), int(s_max)))
+
+    def auto_splits(self, transA, transB, m, n, k, A, lda, B, ldb):
+        out = ct.c_int()
+        _check("ozimmu_auto_splits", lib().ozimmu_auto_splits(
+            self._h, OP[transA], OP[transB], m, n, k, _ptr(A), lda, _ptr(B), ldb, ct.byref(out)))
+        return out.value
 
     def zgemm(self, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_slices):
         """Complex GEMM: A, B, C interleaved complex (e.g. torch.complex128), ld in complex
