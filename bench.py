@@ -280,7 +280,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--slices", type=int, default=None)
+    ap.add_argument("--slices", type=int, default=None,
+                    help="fixed s; 0 = INT8-AUTO with --auto-T (P:656-659)")
+    ap.add_argument("--auto-T", type=float, default=0.0)
     ap.add_argument("--chunk-cols", type=int, default=2048)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -288,7 +290,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     wl = dict(WORKLOADS[args.config])
-    if args.slices:
+    if args.slices is not None:
         wl["s"] = args.slices
     if args.impl == "reference":
         run_reference(args, wl)
@@ -314,6 +316,7 @@ def main():
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     m, n, k, s = wl["m"], wl["n"], wl["k"], wl["s"]
+    s_call = s  # 0 = INT8-AUTO: every step runs the mantissa-loss scan
     r0, r1 = D.row_range(m, world, rank)
     ml = r1 - r0
 
@@ -330,16 +333,18 @@ def main():
     h = oz.Handle(local)
     stream = torch.cuda.current_stream(dev)
     h.set_stream(stream)
+    if s == 0:
+        h.set_auto(args.auto_T, 20)
     be = D.CudaBackend(h, dev)
     bufs = None
 
     def step():
         nonlocal bufs
         if world == 1:
-            h.dgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, s)
+            h.dgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, s_call)
         else:
             bufs = D.dgemm_rowblock(be, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0,
-                                    dC.view(n, ml).t() if ml else dC, lda, s, root=0,
+                                    dC.view(n, ml).t() if ml else dC, lda, s_call, root=0,
                                     chunk_cols=args.chunk_cols, bufs=bufs)
 
     def barrier():
@@ -350,6 +355,9 @@ def main():
         step()
     torch.cuda.synchronize()
     rep = h.report()
+    if s == 0:
+        wl["auto"] = {"T": args.auto_T, "chosen_s": rep["num_slices"]}
+        s = rep["num_slices"]  # for the op counts below; every timed step re-runs the scan
 
     # ---- timed region: inputs resident in HBM -------------------------------------
     h.timing_enable(args.steps + 1)
@@ -513,7 +521,7 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "i8", "data": "synthetic",
         "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "phi": wl["phi"],
-                   "seeds": list(wl["seeds"]),
+                   "seeds": list(wl["seeds"]), "auto": wl.get("auto"),
                    "parallelism": "single GPU" if world == 1 else
                    f"C row blocks x{world} + chunked NCCL broadcast of B slices",
                    "l2": "inputs larger than L2 (each operand 2.1 GB fp64 + 2.4 GB int8 planes)",
