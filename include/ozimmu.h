@@ -175,6 +175,26 @@ OZIMMU_API ozimmu_status_t ozimmu_auto_splits(ozimmu_handle_t h, ozimmu_op_t tra
                                    const double *A, int64_t lda, const double *B, int64_t ldb,
                                    int *num_slices_out);
 
+/* Strided-batched forms (NEXT row f3: the quantum-circuit gate application of P:645-650 as a
+ * batch of matmul-(2^d, 2^o, 2^d) products): C_b = alpha op(A_b) op(B_b) + beta C_b for
+ * b = 0..batch-1, X_b = X + b*strideX (strides in elements: doubles for D, complex for Z).
+ * Each item is bitwise what ozimmu_dgemm / ozimmu_zgemm would return for it.  For D with a
+ * shared op(B) (strideB = 0, num_slices > 0) B is sliced once and its B-slice buffer reused. */
+OZIMMU_API ozimmu_status_t ozimmu_dgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t transA,
+                                             ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                             const double *alpha, const double *A, int64_t lda,
+                                             int64_t strideA, const double *B, int64_t ldb,
+                                             int64_t strideB, const double *beta, double *C,
+                                             int64_t ldc, int64_t strideC, int64_t batch,
+                                             int num_slices);
+OZIMMU_API ozimmu_status_t ozimmu_zgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t transA,
+                                             ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                             const double *alpha, const double *A, int64_t lda,
+                                             int64_t strideA, const double *B, int64_t ldb,
+                                             int64_t strideB, const double *beta, double *C,
+                                             int64_t ldc, int64_t strideC, int64_t batch,
+                                             int num_slices);
+
 /* ---- split-phase entry points (multi-GPU: slice B once, broadcast, reuse) -----
  * A "B-slice buffer" is one contiguous device buffer holding the INT8 planes of
  * the columns of op(B) plus their int32 exponents, in the exact layout the GEMM

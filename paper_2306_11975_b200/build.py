@@ -16,6 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libozimmu.so")
+SHIM = os.path.join(HERE, "libozimmu_cublas_shim.so")
+SHIM_SRC = os.path.join(CSRC, "shim", "cublas_shim.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
@@ -64,6 +66,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _stale(LIB, objs):
         subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB]
                        + objs, check=True)
+    # f3: LD_PRELOAD cuBLAS shim (host C++ only; resolves libozimmu.so next to itself)
+    if force or _stale(SHIM, [SHIM_SRC, LIB] + hdrs):
+        subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-fvisibility=hidden",
+                        "-I", INCLUDE, "-I", "/usr/local/cuda/include", "-o", SHIM, SHIM_SRC,
+                        "-L", HERE, "-lozimmu", "-Wl,-rpath,$ORIGIN", "-ldl"], check=True)
     return LIB
 
 

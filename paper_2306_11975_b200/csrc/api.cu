@@ -806,4 +806,78 @@ ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t 
     return OZIMMU_SUCCESS;
 }
 
+
+// ---- f3: strided-batched forms (cuBLAS-style), quantum-circuit gate application -----------
+
+ozimmu_status_t ozimmu_dgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t transA,
+                                             ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                             const double *alpha, const double *A, int64_t lda,
+                                             int64_t strideA, const double *B, int64_t ldb,
+                                             int64_t strideB, const double *beta, double *C,
+                                             int64_t ldc, int64_t strideC, int64_t batch,
+                                             int num_slices) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (batch < 0 || strideA < 0 || strideB < 0 || strideC < 0) return OZIMMU_ERR_INVALID_VALUE;
+    if (batch == 0) return OZIMMU_SUCCESS;
+    // shared op(B) (strideB == 0), fixed s, real alpha != 0: slice B once, reuse the buffer
+    const bool share_b = strideB == 0 && batch > 1 && num_slices > 0 && alpha && *alpha != 0.0 &&
+                         m > 0 && n > 0 && k > 0;
+    if (share_b) {
+        ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc,
+                                          num_slices);
+        if (st) return st;
+        if (!valid_op(transB) || !B) return OZIMMU_ERR_INVALID_VALUE;
+        if (ldb < ((transB == OZIMMU_OP_N ? k : n) > 1 ? (transB == OZIMMU_OP_N ? k : n) : 1))
+            return OZIMMU_ERR_INVALID_VALUE;
+        if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+        const size_t bb = ozimmu_b_slices_bytes(n, k, num_slices);
+        void *bbuf = nullptr;
+        if (cudaMallocAsync(&bbuf, bb, h->stream) != cudaSuccess) {
+            cudaGetLastError();
+            return OZIMMU_ERR_WORKSPACE;
+        }
+        st = ozimmu_slice_b(h, transB, k, n, B, ldb, num_slices, bbuf);
+        int launches = h->report.launches;
+        for (int64_t b = 0; b < batch && st == OZIMMU_SUCCESS; ++b) {
+            st = ozimmu_dgemm_presliced_b(h, transA, m, n, k, alpha, A + b * strideA, lda, bbuf,
+                                          beta, C + b * strideC, ldc, num_slices);
+            launches += h->report.launches;
+        }
+        cudaFreeAsync(bbuf, h->stream);
+        h->report.launches = launches;
+        return st;
+    }
+    int launches = 0;
+    for (int64_t b = 0; b < batch; ++b) {
+        ozimmu_status_t st = ozimmu_dgemm(h, transA, transB, m, n, k, alpha, A + b * strideA, lda,
+                                          B + b * strideB, ldb, beta, C + b * strideC, ldc,
+                                          num_slices);
+        if (st) return st;
+        launches += h->report.launches;
+    }
+    h->report.launches = launches;
+    return OZIMMU_SUCCESS;
+}
+
+ozimmu_status_t ozimmu_zgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t transA,
+                                             ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                             const double *alpha, const double *A, int64_t lda,
+                                             int64_t strideA, const double *B, int64_t ldb,
+                                             int64_t strideB, const double *beta, double *C,
+                                             int64_t ldc, int64_t strideC, int64_t batch,
+                                             int num_slices) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (batch < 0 || strideA < 0 || strideB < 0 || strideC < 0) return OZIMMU_ERR_INVALID_VALUE;
+    int launches = 0;
+    for (int64_t b = 0; b < batch; ++b) {  // strides in complex elements
+        ozimmu_status_t st = ozimmu_zgemm(h, transA, transB, m, n, k, alpha, A + 2 * b * strideA,
+                                          lda, B + 2 * b * strideB, ldb, beta,
+                                          C + 2 * b * strideC, ldc, num_slices);
+        if (st) return st;
+        launches += h->report.launches;
+    }
+    h->report.launches = launches;
+    return OZIMMU_SUCCESS;
+}
+
 }  // extern "C"

@@ -27,7 +27,8 @@ EXPORTS = [
     "ozimmu_dgemm", "ozimmu_b_slices_bytes", "ozimmu_slice_b", "ozimmu_dgemm_presliced_b",
     "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
     "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
-    "ozimmu_set_auto", "ozimmu_auto_splits",
+    "ozimmu_set_auto", "ozimmu_auto_splits", "ozimmu_dgemm_strided_batched",
+    "ozimmu_zgemm_strided_batched",
 ]
 
 
@@ -86,6 +87,10 @@ def lib():
         "ozimmu_zgemm": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32], i32),
         "ozimmu_zgemm_workspace_bytes": ([i32, i32, i64, i64, i64, i32], sz),
         "ozimmu_set_auto": ([H, ct.c_double, i32], i32),
+        "ozimmu_dgemm_strided_batched": ([H, i32, i32, i64, i64, i64, dp, vp, i64, i64, vp, i64,
+                                          i64, dp, vp, i64, i64, i64, i32], i32),
+        "ozimmu_zgemm_strided_batched": ([H, i32, i32, i64, i64, i64, dp, vp, i64, i64, vp, i64,
+                                          i64, dp, vp, i64, i64, i64, i32], i32),
         "ozimmu_auto_splits": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, ct.POINTER(i32)], i32),
         "ozimmu_timing_read": ([H, ct.POINTER(Timing), i32], i32),
     }
@@ -204,6 +209,20 @@ class Handle:
         _check("ozimmu_zgemm", lib().ozimmu_zgemm(
             self._h, OP[transA], OP[transB], m, n, k, a, _ptr(A), lda, _ptr(B), ldb, b, _ptr(C),
             ldc, int(num_slices)))
+
+    def dgemm_strided_batched(self, transA, transB, m, n, k, alpha, A, lda, strideA, B, ldb,
+                              strideB, beta, C, ldc, strideC, batch, num_slices):
+        _check("ozimmu_dgemm_strided_batched", lib().ozimmu_dgemm_strided_batched(
+            self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _ptr(A), lda, strideA, _ptr(B),
+            ldb, strideB, _d(beta), _ptr(C), ldc, strideC, batch, int(num_slices)))
+
+    def zgemm_strided_batched(self, transA, transB, m, n, k, alpha, A, lda, strideA, B, ldb,
+                              strideB, beta, C, ldc, strideC, batch, num_slices):
+        a = (ct.c_double * 2)(complex(alpha).real, complex(alpha).imag)
+        b = (ct.c_double * 2)(complex(beta).real, complex(beta).imag)
+        _check("ozimmu_zgemm_strided_batched", lib().ozimmu_zgemm_strided_batched(
+            self._h, OP[transA], OP[transB], m, n, k, a, _ptr(A), lda, strideA, _ptr(B), ldb,
+            strideB, b, _ptr(C), ldc, strideC, batch, int(num_slices)))
 
     def slice_b(self, transB, k, n, B, ldb, num_slices, b_slices):
         _check("ozimmu_slice_b", lib().ozimmu_slice_b(

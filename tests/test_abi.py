@@ -73,3 +73,18 @@ def test_null_handle_validation():
     assert L.ozimmu_dgemm(None, 0, 0, 4, 4, 4, one, 1, 4, 1, 4, one, 1, 4, 9) == 5
     assert L.ozimmu_set_stream(None, None) == 5
     assert L.ozimmu_destroy(None) == 0
+
+
+def test_cublas_shim_exports():
+    """NEXT row f3: the LD_PRELOAD shim defines exactly the cuBLAS GEMMs it interposes and
+    loads without a GPU (resolving libozimmu.so next to itself)."""
+    import ctypes
+    import subprocess
+    shim = os.path.join(os.path.dirname(B.__file__), "libozimmu_cublas_shim.so")
+    assert os.path.exists(shim), "run __graft_entry__.build()"
+    out = subprocess.run(["nm", "-D", "--defined-only", shim], capture_output=True, text=True,
+                         check=True).stdout
+    defined = sorted(l.split()[-1] for l in out.splitlines() if " T " in l)
+    assert defined == sorted(["cublasDgemm_v2", "cublasZgemm_v2", "cublasDgemmStridedBatched",
+                              "cublasZgemmStridedBatched"])
+    ctypes.CDLL(shim)
