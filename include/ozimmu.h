@@ -142,6 +142,24 @@ OZIMMU_API ozimmu_status_t ozimmu_dgemm(ozimmu_handle_t h, ozimmu_op_t transA, o
                              const double *A, int64_t lda, const double *B, int64_t ldb,
                              const double *beta, double *C, int64_t ldc, int num_slices);
 
+/* As ozimmu_dgemm with A, B and C in HOST memory (the call a host program makes; BJ
+ * metric "including the matrix splitting" end to end).  Pinned (cudaHostAlloc /
+ * cudaHostRegister) buffers overlap the PCIe copies with the computation; pageable buffers
+ * work but serialise.  op(A) is processed in row blocks and op(B) in column chunks: the H2D
+ * copies, the slicing of each chunk, the GEMM of each block and the D2H copy of each C
+ * block run on three streams (the handle's stream + two internal copy streams), so tensor
+ * work starts after the first chunk arrives.  C is bitwise identical to ozimmu_dgemm on the
+ * same data.  num_slices = 0 (INT8-AUTO) copies both operands before choosing s (no
+ * overlap).  Device memory: an internal buffer (grown on demand, freed by ozimmu_destroy)
+ * of about s(n + 2 m/8) k_pad + 8 k (2 n/8 + 2 m/8) + 16 (m/8) n bytes.  The call BLOCKS
+ * until C is in host memory.  Errors: as ozimmu_dgemm; WORKSPACE if the buffer cannot be
+ * allocated. */
+OZIMMU_API ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t transA,
+                                  ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                  const double *alpha, const double *A, int64_t lda,
+                                  const double *B, int64_t ldb, const double *beta, double *C,
+                                  int64_t ldc, int num_slices);
+
 /* Complex GEMM (NEXT row f1; "separating the real and imaginary parts ... while
  * splitting").  Complex numbers are interleaved (re, im) doubles (cuDoubleComplex layout);
  * lda / ldb / ldc count complex elements; alpha and beta point to 2 doubles (re, im);

@@ -29,6 +29,10 @@ struct ozimmu_ctx {
     int auto_smax = 20;
     int auto_last_s = 0;
     unsigned long long *auto_dev = nullptr;  // device [2][33] loss sums
+    // host-buffer entry point (ozimmu_dgemm_host): copy streams + device staging buffer
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    void *host_buf = nullptr;
+    size_t host_buf_bytes = 0;
 };
 
 namespace {
@@ -250,6 +254,56 @@ ozimmu_status_t auto_select(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t t
     return OZIMMU_SUCCESS;
 }
 
+// The fused tcgen05 GEMM + FP64 epilogue (A4 + A5) on sliced operands.  b_plane_rows: rows
+// per B plane in memory (0 = n; a column chunk of a wider B-slice buffer otherwise).
+cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t n, int64_t k_pad,
+                       int s, int w, const int8_t *a_planes, const int32_t *EA,
+                       const int8_t *b_planes, const int32_t *EB, int64_t b_plane_rows,
+                       double alpha, double beta, double *C, int64_t ldc, int64_t *scratch,
+                       unsigned int *sync, int *launches) {
+    GemmArgs ga{};
+    ga.a_planes = a_planes;
+    ga.b_planes = b_planes;
+    ga.b_plane_rows = b_plane_rows;
+    ga.EA = EA;
+    ga.EB = EB;
+    ga.m = m;
+    ga.n = n;
+    ga.k_pad = k_pad;
+    ga.s = s;
+    ga.w = w;
+    ga.alpha = alpha;
+    ga.beta = beta;
+    ga.C = C;
+    ga.ldc = ldc;
+    ga.chunk_scratch = scratch;
+    // soft per-wave grid barrier (L2 reuse); OZIMMU_NO_WAVE_SYNC=1 disables (experiments)
+    static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
+    ga.wave_counter = no_sync ? nullptr : sync;
+    // development instrumentation: OZIMMU_STATS=1 -> per-CTA stall counters, dumped below
+    static const bool want_stats = getenv("OZIMMU_STATS") != nullptr;
+    static long long *stats_buf = nullptr;
+    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 12 * 1024 * sizeof(long long));
+    ga.stats = want_stats ? stats_buf : nullptr;
+    cudaError_t e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, launches);
+    if (e != cudaSuccess || !ga.stats) return e;
+    // development only: synchronous dump of the stall counters
+    constexpr int NS = 12;
+    static long long host[NS * 1024];
+    cudaStreamSynchronize(h->stream);
+    cudaMemcpy(host, ga.stats, sizeof(long long) * NS * gp.grid, cudaMemcpyDeviceToHost);
+    double acc[NS] = {0};
+    for (int c = 0; c < gp.grid; ++c)
+        for (int i = 0; i < NS; ++i) acc[i] += (double)host[c * NS + i];
+    const char *names[NS] = {"total", "mma_wait_b", "mma_wait_a", "mma_wait_tmem", "prod_wave",
+                             "prod_wait_a", "prod_wait_b", "epi_busy", "epi_tmem", "epi_store",
+                             "mma_wait_a_first_kb", "mma_wait_b_kb0"};
+    fprintf(stderr, "[ozimmu stats] grid=%d avg cycles:", gp.grid);
+    for (int i = 0; i < NS; ++i) fprintf(stderr, " %s=%.0f", names[i], acc[i] / gp.grid);
+    fprintf(stderr, "\n");
+    return cudaSuccess;
+}
+
 ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t n, int64_t k,
                           double alpha, const double *A, int64_t lda, const uint8_t *bbuf_ext,
                           ozimmu_op_t transB, const double *B, int64_t ldb, double beta,
@@ -281,49 +335,13 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 2);
-    GemmArgs ga{};
-    ga.a_planes = a_planes;
-    ga.b_planes = reinterpret_cast<const int8_t *>(bbuf);
-    ga.EA = EA;
-    ga.EB = reinterpret_cast<const int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
-    ga.m = m;
-    ga.n = n;
-    ga.k_pad = k_pad;
-    ga.s = s;
-    ga.w = w;
-    ga.alpha = alpha;
-    ga.beta = beta;
-    ga.C = C;
-    ga.ldc = ldc;
-    ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
-    // soft per-wave grid barrier (L2 reuse); OZIMMU_NO_WAVE_SYNC=1 disables (experiments)
-    static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
-    ga.wave_counter = no_sync ? nullptr : reinterpret_cast<unsigned int *>(base + L.sync);
-    // development instrumentation: OZIMMU_STATS=1 -> per-CTA stall counters, printed by
-    // ozimmu_debug_print_stats via the environment-only hook below
-    static const bool want_stats = getenv("OZIMMU_STATS") != nullptr;
-    static long long *stats_buf = nullptr;
-    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 12 * 1024 * sizeof(long long));
-    ga.stats = want_stats ? stats_buf : nullptr;
-    e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, &launches);
+    e = fused_gemm(h, gp, m, n, k_pad, s, w, a_planes, EA, reinterpret_cast<const int8_t *>(bbuf),
+                   reinterpret_cast<const int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s)), 0,
+                   alpha, beta, C, ldc, reinterpret_cast<int64_t *>(base + L.scratch),
+                   reinterpret_cast<unsigned int *>(base + L.sync), &launches);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 3);
     mark_done(h);
-    if (ga.stats) {  // development only: synchronous dump of the stall counters
-        constexpr int NS = 12;
-        static long long host[NS * 1024];
-        cudaStreamSynchronize(h->stream);
-        cudaMemcpy(host, ga.stats, sizeof(long long) * NS * gp.grid, cudaMemcpyDeviceToHost);
-        double acc[NS] = {0};
-        for (int c = 0; c < gp.grid; ++c)
-            for (int i = 0; i < NS; ++i) acc[i] += (double)host[c * NS + i];
-        const char *names[NS] = {"total", "mma_wait_b", "mma_wait_a", "mma_wait_tmem", "prod_wave",
-                                 "prod_wait_a", "prod_wait_b", "epi_busy", "epi_tmem", "epi_store",
-                                 "mma_wait_a_first_kb", "mma_wait_b_kb0"};
-        fprintf(stderr, "[ozimmu stats] grid=%d avg cycles:", gp.grid);
-        for (int i = 0; i < NS; ++i) fprintf(stderr, " %s=%.0f", names[i], acc[i] / gp.grid);
-        fprintf(stderr, "\n");
-    }
     fill_report(h, s, w, m, n, k, &gp, launches, slice_bytes);
     return OZIMMU_SUCCESS;
 }
@@ -448,6 +466,12 @@ ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
         cudaStreamSynchronize(h->stream);
         cudaFree(h->own_ws);
     }
+    if (h->host_buf) {
+        cudaDeviceSynchronize();
+        cudaFree(h->host_buf);
+    }
+    if (h->h2d) cudaStreamDestroy(h->h2d);
+    if (h->d2h) cudaStreamDestroy(h->d2h);
     delete h;
     return OZIMMU_SUCCESS;
 }
@@ -881,3 +905,283 @@ ozimmu_status_t ozimmu_zgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t tran
 }
 
 }  // extern "C"
+
+
+// ---- host-buffer entry point: H2D copies, slicing, GEMM and D2H overlapped ----------------
+//
+// op(A) is cut into row blocks A_0..A_{P-1} and op(B) into column chunks B_0..B_{J-1}.  Copy
+// order on the H2D stream: A_0, B_0..B_{J-1}, A_1, .., A_{P-1}; compute stream: slice A_0, then
+// per chunk j slice B_j into the full B-slice buffer and run GEMM(A_0, B_j) (so tensor work
+// starts after the first chunk, not after all of B), then per block i >= 1 slice A_i and run
+// GEMM(A_i, B) on the whole B-slice buffer; the D2H stream returns C block i as soon as its
+// GEMM ends.  Every element of C sees the same operation sequence as ozimmu_dgemm (rows of
+// op(A) and columns of op(B) are sliced independently; the epilogue is per element), so the
+// result is bitwise identical to the device-pointer call.  Staging slots are double-buffered
+// with events; the call blocks until C is back in host memory.
+namespace {
+
+struct HostPlan {
+    int64_t mb, nb, P, J;
+    size_t bbuf, bst, ast, apl, cst, keys, sync, scratch, total;
+    size_t o_bbuf, o_bst[2], o_ast[2], o_apl[2], o_cst[2], o_keys, o_sync, o_scratch;
+};
+
+bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPlan *hp) {
+    const int w = slice_width(k);
+    const int64_t k_pad = round_up(k, 16);
+    static const int64_t env_mb = getenv("OZIMMU_HOST_MB") ? atoll(getenv("OZIMMU_HOST_MB")) : 0;
+    static const int64_t env_nb = getenv("OZIMMU_HOST_NB") ? atoll(getenv("OZIMMU_HOST_NB")) : 0;
+    int64_t mb = env_mb > 0 ? env_mb : round_up(ceil_div(m, 8), 128);
+    int64_t nb = env_nb > 0 ? env_nb : round_up(ceil_div(n, 8), 64);
+    if (mb < 512) mb = 512;
+    if (nb < 512) nb = 512;
+    if (mb > m) mb = m;
+    if (nb > n) nb = n;
+    hp->mb = mb;
+    hp->nb = nb;
+    hp->P = ceil_div(m, mb);
+    hp->J = ceil_div(n, nb);
+    size_t scratch = 0;
+    const int64_t shapes[3][2] = {{mb, nb}, {mb, n}, {m - (hp->P - 1) * mb, n}};
+    for (auto &sh : shapes) {
+        GemmPlan gp;
+        if (!plan_gemm(s, w, sh[0], sh[1], k_pad, h->num_sms, &gp)) return false;
+        const size_t c = chunk_scratch_bytes(gp, s);
+        if (c > scratch) scratch = c;
+    }
+    hp->bbuf = b_buf_bytes(n, k_pad, s);
+    hp->bst = align_up((size_t)k * nb * sizeof(double));
+    hp->ast = align_up((size_t)mb * k * sizeof(double));
+    hp->apl = align_up((size_t)s * mb * k_pad) + align_up(sizeof(int32_t) * (size_t)mb);
+    hp->cst = align_up((size_t)mb * n * sizeof(double));
+    hp->keys = align_up(sizeof(int32_t) * (size_t)(mb > nb ? mb : nb));
+    hp->sync = kAlign;
+    hp->scratch = align_up(scratch);
+    size_t off = 0;
+    hp->o_bbuf = off; off += hp->bbuf;
+    for (int i = 0; i < 2; ++i) { hp->o_bst[i] = off; off += hp->bst; }
+    for (int i = 0; i < 2; ++i) { hp->o_ast[i] = off; off += hp->ast; }
+    for (int i = 0; i < 2; ++i) { hp->o_apl[i] = off; off += hp->apl; }
+    for (int i = 0; i < 2; ++i) { hp->o_cst[i] = off; off += hp->cst; }
+    hp->o_keys = off; off += hp->keys;
+    hp->o_sync = off; off += hp->sync;
+    hp->o_scratch = off; off += hp->scratch;
+    hp->total = off;
+    return true;
+}
+
+ozimmu_status_t host_buffers(ozimmu_handle_t h, size_t need) {
+    if (!h->h2d && cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking) != cudaSuccess)
+        return cuda_status(cudaErrorUnknown);
+    if (!h->d2h && cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking) != cudaSuccess)
+        return cuda_status(cudaErrorUnknown);
+    if (need <= h->host_buf_bytes) return OZIMMU_SUCCESS;
+    if (h->host_buf) {
+        cudaDeviceSynchronize();
+        cudaFree(h->host_buf);
+        h->host_buf = nullptr;
+        h->host_buf_bytes = 0;
+    }
+    if (cudaMalloc(&h->host_buf, need) != cudaSuccess) {
+        cudaGetLastError();
+        return OZIMMU_ERR_WORKSPACE;
+    }
+    h->host_buf_bytes = need;
+    return OZIMMU_SUCCESS;
+}
+
+// 2-D column-major copy: `cols` columns of `rows` doubles, leading dimensions in doubles.
+inline cudaError_t copy2d(double *dst, int64_t ldd, const double *src, int64_t lds, int64_t rows,
+                          int64_t cols, cudaMemcpyKind kind, cudaStream_t st) {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    return cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double),
+                             rows * sizeof(double), cols, kind, st);
+}
+
+// Non-pipelined host path (INT8-AUTO needs both operands on the device before s is known;
+// degenerate alpha = 0 / k = 0 calls): copy in, ozimmu_dgemm, copy out.
+ozimmu_status_t host_full(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
+                          int64_t n, int64_t k, const double *alpha, const double *A, int64_t lda,
+                          const double *B, int64_t ldb, const double *beta, double *C,
+                          int64_t ldc, int num_slices) {
+    const bool use_ab = *alpha != 0.0 && k > 0;
+    const int64_t ar = transA == OZIMMU_OP_N ? m : k, ac = transA == OZIMMU_OP_N ? k : m;
+    const int64_t br = transB == OZIMMU_OP_N ? k : n, bc = transB == OZIMMU_OP_N ? n : k;
+    const size_t sa = use_ab ? align_up(sizeof(double) * (size_t)ar * ac) : 0;
+    const size_t sb = use_ab ? align_up(sizeof(double) * (size_t)br * bc) : 0;
+    const size_t sc = align_up(sizeof(double) * (size_t)m * n);
+    ozimmu_status_t st = host_buffers(h, sa + sb + sc);
+    if (st) return st;
+    uint8_t *base = static_cast<uint8_t *>(h->host_buf);
+    double *dA = reinterpret_cast<double *>(base), *dB = reinterpret_cast<double *>(base + sa);
+    double *dC = reinterpret_cast<double *>(base + sa + sb);
+    cudaError_t e = cudaSuccess;
+    if (use_ab) {
+        e = copy2d(dA, ar, A, lda, ar, ac, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess) e = copy2d(dB, br, B, ldb, br, bc, cudaMemcpyHostToDevice, h->stream);
+    }
+    if (e == cudaSuccess && *beta != 0.0)
+        e = copy2d(dC, m, C, ldc, m, n, cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    st = ozimmu_dgemm(h, transA, transB, m, n, k, alpha, use_ab ? dA : nullptr, ar > 1 ? ar : 1,
+                      use_ab ? dB : nullptr, br > 1 ? br : 1, beta, dC, m > 1 ? m : 1, num_slices);
+    if (st) return st;
+    e = copy2d(C, ldc, dC, m, m, n, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    return cuda_status(e);
+}
+
+}  // namespace
+
+extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t transA,
+                                             ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
+                                             const double *alpha, const double *A, int64_t lda,
+                                             const double *B, int64_t ldb, const double *beta,
+                                             double *C, int64_t ldc, int num_slices) {
+    ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc, num_slices);
+    if (st) return st;
+    if (!valid_op(transB)) return OZIMMU_ERR_INVALID_VALUE;
+    const int64_t brows = transB == OZIMMU_OP_N ? k : n;
+    if (ldb < (brows > 1 ? brows : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (n > 0 && k > 0 && m > 0 && *alpha != 0.0 && !B) return OZIMMU_ERR_INVALID_VALUE;
+    if (m == 0 || n == 0) {
+        fill_report(h, 0, 0, m, n, k, nullptr, 0, 0);
+        return OZIMMU_SUCCESS;
+    }
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    if (num_slices == 0 || *alpha == 0.0 || k == 0)
+        return host_full(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                         num_slices);
+    const int s = num_slices;
+    const int w = slice_width(k);
+    const int64_t k_pad = round_up(k, 16);
+    HostPlan hp;
+    if (!host_plan(h, m, n, k, s, &hp)) return OZIMMU_ERR_UNSUPPORTED;
+    st = host_buffers(h, hp.total);
+    if (st) return st;
+    uint8_t *base = static_cast<uint8_t *>(h->host_buf);
+    uint8_t *bbuf = base + hp.o_bbuf;
+    int8_t *b_planes = reinterpret_cast<int8_t *>(bbuf);
+    int32_t *EB = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
+    int32_t *keys = reinterpret_cast<int32_t *>(base + hp.o_keys);
+    int64_t *scratch = reinterpret_cast<int64_t *>(base + hp.o_scratch);
+    unsigned int *sync = reinterpret_cast<unsigned int *>(base + hp.o_sync);
+    const bool has_beta = *beta != 0.0;
+    const bool a_rows_contig = transA != OZIMMU_OP_N;  // device copy of a row block
+    const bool b_cols_contig = transB == OZIMMU_OP_N;
+
+    // events: [0] start, then per block / chunk
+    const int64_t P = hp.P, J = hp.J;
+    const int64_t n_ev = 1 + 5 * P + 2 * J;
+    cudaEvent_t *ev = static_cast<cudaEvent_t *>(calloc((size_t)n_ev, sizeof(cudaEvent_t)));
+    if (!ev) return OZIMMU_ERR_WORKSPACE;
+    cudaError_t e = cudaSuccess;
+    int64_t made = 0;
+    for (; made < n_ev && e == cudaSuccess; ++made)
+        e = cudaEventCreateWithFlags(&ev[made], cudaEventDisableTiming);
+    cudaEvent_t ev_start = ev[0];
+    cudaEvent_t *ev_ain = ev + 1, *ev_afree = ev + 1 + P, *ev_cin = ev + 1 + 2 * P;
+    cudaEvent_t *ev_cdone = ev + 1 + 3 * P, *ev_cout = ev + 1 + 4 * P;
+    cudaEvent_t *ev_bin = ev + 1 + 5 * P, *ev_bfree = ev + 1 + 5 * P + J;
+    int launches = 0;
+    cudaStream_t cs = h->stream;
+#define OZ_TRY(x) do { if (e == cudaSuccess) e = (x); } while (0)
+    OZ_TRY(cudaEventRecord(ev_start, cs));
+    OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_start, 0));
+    OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_start, 0));
+
+    auto block_rows = [&](int64_t i) { return (i == P - 1) ? m - i * hp.mb : hp.mb; };
+    auto copy_a = [&](int64_t i) {
+        const int64_t r0 = i * hp.mb, mi = block_rows(i);
+        double *dst = reinterpret_cast<double *>(base + hp.o_ast[i & 1]);
+        if (i >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_afree[i - 2], 0));
+        if (a_rows_contig)  // stored k x m: columns r0 .. r0+mi
+            OZ_TRY(copy2d(dst, k, A + r0 * lda, lda, k, mi, cudaMemcpyHostToDevice, h->h2d));
+        else  // stored m x k: rows r0 .. r0+mi of every column
+            OZ_TRY(copy2d(dst, mi, A + r0, lda, mi, k, cudaMemcpyHostToDevice, h->h2d));
+        OZ_TRY(cudaEventRecord(ev_ain[i], h->h2d));
+        if (has_beta) {
+            if (i >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_cout[i - 2], 0));
+            OZ_TRY(copy2d(reinterpret_cast<double *>(base + hp.o_cst[i & 1]), mi, C + r0, ldc, mi,
+                          n, cudaMemcpyHostToDevice, h->h2d));
+            OZ_TRY(cudaEventRecord(ev_cin[i], h->h2d));
+        }
+    };
+    auto slice_a_block = [&](int64_t i) {
+        const int64_t mi = block_rows(i);
+        const double *src = reinterpret_cast<const double *>(base + hp.o_ast[i & 1]);
+        int8_t *pl = reinterpret_cast<int8_t *>(base + hp.o_apl[i & 1]);
+        int32_t *EA = reinterpret_cast<int32_t *>(base + hp.o_apl[i & 1] +
+                                                  align_up((size_t)s * hp.mb * k_pad));
+        OZ_TRY(cudaStreamWaitEvent(cs, ev_ain[i], 0));
+        OZ_TRY(launch_split(src, a_rows_contig ? k : mi, a_rows_contig, mi, k, k_pad, s, w,
+                            /*reverse=*/false, pl, mi * k_pad, EA, keys, h->num_sms, cs,
+                            &launches));
+        OZ_TRY(cudaEventRecord(ev_afree[i], cs));
+        if (has_beta) OZ_TRY(cudaStreamWaitEvent(cs, ev_cin[i], 0));
+        else if (i >= 2) OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[i - 2], 0));
+    };
+    auto gemm = [&](int64_t i, int64_t c0, int64_t nc) {
+        const int64_t mi = block_rows(i);
+        const int8_t *pl = reinterpret_cast<const int8_t *>(base + hp.o_apl[i & 1]);
+        const int32_t *EA = reinterpret_cast<const int32_t *>(base + hp.o_apl[i & 1] +
+                                                              align_up((size_t)s * hp.mb * k_pad));
+        double *dC = reinterpret_cast<double *>(base + hp.o_cst[i & 1]);
+        GemmPlan gp;
+        if (!plan_gemm(s, w, mi, nc, k_pad, h->num_sms, &gp)) {
+            if (e == cudaSuccess) e = cudaErrorInvalidValue;
+            return;
+        }
+        OZ_TRY(fused_gemm(h, gp, mi, nc, k_pad, s, w, pl, EA, b_planes + c0 * k_pad, EB + c0, n,
+                          *alpha, *beta, dC + c0 * mi, mi, scratch, sync, &launches));
+    };
+    auto copy_c_out = [&](int64_t i) {
+        const int64_t mi = block_rows(i);
+        OZ_TRY(cudaEventRecord(ev_cdone[i], cs));
+        OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_cdone[i], 0));
+        OZ_TRY(copy2d(C + i * hp.mb, ldc, reinterpret_cast<const double *>(base + hp.o_cst[i & 1]),
+                      mi, mi, n, cudaMemcpyDeviceToHost, h->d2h));
+        OZ_TRY(cudaEventRecord(ev_cout[i], h->d2h));
+    };
+
+    copy_a(0);
+    slice_a_block(0);
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t c0 = j * hp.nb, nc = (j == J - 1) ? n - c0 : hp.nb;
+        double *dst = reinterpret_cast<double *>(base + hp.o_bst[j & 1]);
+        if (j >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_bfree[j - 2], 0));
+        if (b_cols_contig)  // stored k x n: columns c0 .. c0+nc
+            OZ_TRY(copy2d(dst, k, B + c0 * ldb, ldb, k, nc, cudaMemcpyHostToDevice, h->h2d));
+        else  // stored n x k: rows c0 .. c0+nc
+            OZ_TRY(copy2d(dst, nc, B + c0, ldb, nc, k, cudaMemcpyHostToDevice, h->h2d));
+        OZ_TRY(cudaEventRecord(ev_bin[j], h->h2d));
+        OZ_TRY(cudaStreamWaitEvent(cs, ev_bin[j], 0));
+        OZ_TRY(launch_split(dst, b_cols_contig ? k : nc, b_cols_contig, nc, k, k_pad, s, w,
+                            /*reverse=*/true, b_planes + c0 * k_pad, n * k_pad, EB + c0, keys,
+                            h->num_sms, cs, &launches));
+        OZ_TRY(cudaEventRecord(ev_bfree[j], cs));
+        gemm(0, c0, nc);
+    }
+    copy_c_out(0);
+    for (int64_t i = 1; i < P; ++i) {
+        copy_a(i);
+        slice_a_block(i);
+        gemm(i, 0, n);
+        copy_c_out(i);
+    }
+    OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[P - 1], 0));
+    OZ_TRY(cudaStreamSynchronize(cs));
+#undef OZ_TRY
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(h->h2d);
+        cudaStreamSynchronize(h->d2h);
+        cudaStreamSynchronize(cs);
+    }
+    for (int64_t i = 0; i < made; ++i) cudaEventDestroy(ev[i]);
+    free(ev);
+    if (e != cudaSuccess) return cuda_status(e);
+    GemmPlan gp;
+    plan_gemm(s, w, hp.mb, n, k_pad, h->num_sms, &gp);
+    fill_report(h, s, w, m, n, k, &gp, launches, (int64_t)s * (m + n) * k_pad + 4 * (m + n));
+    return OZIMMU_SUCCESS;
+}

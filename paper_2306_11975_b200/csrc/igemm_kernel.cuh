@@ -576,12 +576,15 @@ inline PFN_encodeTiled get_encode() {
 
 // 3-D map over planes [s][rows][k_pad] (int8, K contiguous), 128B swizzle, box
 // (128 B of K, box_rows rows, box_s slices).
+// plane_rows (>= rows, 0 = rows): rows per plane in memory, so a window of rows of a larger
+// buffer (a column chunk of a B-slice buffer) can be addressed in place.
 inline bool make_map(CUtensorMap *map, const int8_t *base, int64_t k_pad, int64_t rows, int s,
-              uint32_t box_rows, uint32_t box_s) {
+              uint32_t box_rows, uint32_t box_s, int64_t plane_rows = 0) {
     PFN_encodeTiled enc = get_encode();
     if (!enc) return false;
+    if (plane_rows < rows) plane_rows = rows;
     cuuint64_t dims[3] = {(cuuint64_t)k_pad, (cuuint64_t)rows, (cuuint64_t)s};
-    cuuint64_t strides[2] = {(cuuint64_t)k_pad, (cuuint64_t)(k_pad * rows)};
+    cuuint64_t strides[2] = {(cuuint64_t)k_pad, (cuuint64_t)(k_pad * plane_rows)};
     cuuint32_t box[3] = {(cuuint32_t)kKB, box_rows, box_s};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t *>(base), dims,
@@ -596,7 +599,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     constexpr int NC = nc_for(S);
     CUtensorMap tmA, tmB;
     if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, kBlockM, 1)) return cudaErrorInvalidValue;
-    if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s))
+    if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s, a.b_plane_rows))
         return cudaErrorInvalidValue;
     CUtensorMap tmApf;  // up to 8 A-slice tiles of a k-block per box (L2 prefetch only)
     if (!make_map(&tmApf, a.a_planes, a.k_pad, a.m, a.s, kBlockM, (uint32_t)(a.s < 8 ? a.s : 8)))

@@ -51,6 +51,7 @@ enum EpiMode : int { EPI_DGEMM = 0, EPI_LEVELS_I64 = 1, EPI_PAIR_I32 = 2, EPI_ZG
 struct GemmArgs {
     const int8_t *a_planes;  // [s][m][k_pad], natural slice order
     const int8_t *b_planes;  // [s][n][k_pad], REVERSED slice order (index s - q)
+    int64_t b_plane_rows;    // rows per B plane in memory (0 = n): column chunk of a larger buffer
     const int32_t *EA, *EB;  // exponents (EPI_DGEMM only)
     int64_t m, n, k_pad;
     int s, w;

@@ -28,7 +28,7 @@ EXPORTS = [
     "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
     "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
     "ozimmu_set_auto", "ozimmu_auto_splits", "ozimmu_dgemm_strided_batched",
-    "ozimmu_zgemm_strided_batched",
+    "ozimmu_zgemm_strided_batched", "ozimmu_dgemm_host",
 ]
 
 
@@ -77,6 +77,8 @@ def lib():
         "ozimmu_version": ([], i32),
         "ozimmu_status_string": ([i32], ct.c_char_p),
         "ozimmu_dgemm": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32], i32),
+        "ozimmu_dgemm_host": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32],
+                              i32),
         "ozimmu_b_slices_bytes": ([i64, i64, i32], sz),
         "ozimmu_slice_b": ([H, i32, i64, i64, vp, i64, i32, vp], i32),
         "ozimmu_dgemm_presliced_b": ([H, i32, i64, i64, i64, dp, vp, i64, vp, dp, vp, i64, i32], i32),
@@ -109,6 +111,16 @@ def _check(fn, rc):
 
 def _d(x):
     return ct.byref(ct.c_double(float(x)))
+
+
+def _hptr(t):
+    """Host address of a CPU torch tensor, a numpy array or an int."""
+    if t is None or isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        assert not t.is_cuda, "ozimmu_dgemm_host takes host buffers"
+        return t.data_ptr()
+    return t.ctypes.data
 
 
 def _ptr(t):
@@ -190,6 +202,14 @@ class Handle:
         _check("ozimmu_dgemm", lib().ozimmu_dgemm(
             self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _ptr(A), lda, _ptr(B), ldb,
             _d(beta), _ptr(C), ldc, int(num_slices)))
+
+    def dgemm_host(self, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                   num_slices):
+        """ozimmu_dgemm with A, B, C in host memory (CPU torch tensors, pinned for overlap,
+        or numpy arrays / raw addresses); blocks until C is written."""
+        _check("ozimmu_dgemm_host", lib().ozimmu_dgemm_host(
+            self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _hptr(A), lda, _hptr(B), ldb,
+            _d(beta), _hptr(C), ldc, int(num_slices)))
 
     def set_auto(self, threshold, s_max=20):
         """INT8-AUTO settings for num_slices = 0 calls."""
