@@ -10,6 +10,15 @@
 // These kernels accumulate, for s = 1..s_max, the exact integer sum of loss_s over the
 // nonzero finite elements of the rows of op(A) / columns of op(B), plus their count; the
 // host then picks the smallest s whose mean loss is <= T for both operands.
+//
+// Evaluation (exact, no loop over s per element).  With l = t_last - vlen,
+//     loss_s(x) = max(0, t_last - s w) - max(0, l - s w)
+// (min(max(0, a), v) = max(0, a) - max(0, a - v) for v >= 0), and for an integer y,
+// max(0, y - s w) > 0 exactly for 1 <= s <= q(y) = (y - 1) div w (y >= 1), so
+//     sum_x loss_s(x) = F(s),  F(s) = sum_{y: q(y) >= s} c_y y  -  s w sum_{y: q(y) >= s} c_y
+// over the multiset of y = t_last (c = +1) and y = l (c = -1).  Each thread bins its
+// elements by q' = min(q, s_max) into a signed count and a signed sum held in its own
+// shared-memory column; suffix sums over q' give its F(s) for every s.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -43,121 +52,167 @@ __device__ __forceinline__ void bit_span(double x, int32_t E, int &t_last, int &
     t_last = E - (e0 + tz);                              // position of the lowest set bit
 }
 
-template <int S_MAX>
-__device__ __forceinline__ void add_loss(double x, int32_t E, int w, int s_max,
-                                         uint32_t (&acc)[S_MAX], uint32_t &cnt) {
-    if (x == 0.0) return;
-    int t_last, vlen;
-    bit_span(x, E, t_last, vlen);
-    ++cnt;
-#pragma unroll
-    for (int s = 1; s <= S_MAX; ++s) {
-        if (s > s_max) break;
-        int over = t_last - s * w;
-        over = over < 0 ? 0 : (over > vlen ? vlen : over);
-        acc[s - 1] += (uint32_t)over;
+// Per-thread histogram columns in dynamic shared memory:
+//   cnt[q' - 1][tid], ysum[q' - 1][tid] (int32, q' = 1..s_max), then the division table
+//   qtab[y - 1] = min((y - 1) div w, s_max) for y - 1 in [0, s_max w].
+struct LossHist {
+    int32_t *cnt, *ysum;
+    const uint8_t *qtab;
+    int w, s_max, lim;
+    uint32_t nnz;
+
+    __device__ __forceinline__ void bin(int y, int c) {
+        if (y <= w) return;  // q(y) = 0: no s >= 1 sees it
+        const int q = qtab[min(y - 1, lim)];
+        const int i = (q - 1) * blockDim.x + threadIdx.x;
+        cnt[i] += c;
+        ysum[i] += c * y;
     }
+    __device__ __forceinline__ void add(double x, int32_t E) {
+        if (x == 0.0) return;
+        int t_last, vlen;
+        bit_span(x, E, t_last, vlen);
+        ++nnz;
+        bin(t_last, 1);
+        bin(t_last - vlen, -1);
+    }
+};
+
+__device__ __forceinline__ LossHist hist_init(int w, int s_max) {
+    extern __shared__ int32_t sh[];
+    LossHist H;
+    H.cnt = sh;
+    H.ysum = sh + s_max * blockDim.x;
+    uint8_t *qt = reinterpret_cast<uint8_t *>(sh + 2 * s_max * blockDim.x);
+    H.w = w;
+    H.s_max = s_max;
+    H.lim = s_max * w;
+    H.nnz = 0;
+    for (int i = threadIdx.x; i <= H.lim; i += blockDim.x) qt[i] = (uint8_t)min(i / w, s_max);
+    for (int q = 0; q < s_max; ++q) {
+        H.cnt[q * blockDim.x + threadIdx.x] = 0;
+        H.ysum[q * blockDim.x + threadIdx.x] = 0;
+    }
+    H.qtab = qt;
+    __syncthreads();
+    return H;
 }
 
-// Block-reduce the per-thread sums and add them to out[0..s_max) (int64) and out[kMaxS].
-template <int S_MAX>
-__device__ __forceinline__ void flush(const uint32_t (&acc)[S_MAX], uint32_t cnt, int s_max,
-                                      unsigned long long *out) {
-    __shared__ unsigned long long red[S_MAX + 1];
-    if (threadIdx.x <= S_MAX) red[threadIdx.x] = 0;
+size_t hist_smem(int s_max, int threads, int w) {
+    return sizeof(int32_t) * 2 * (size_t)s_max * threads + (size_t)(s_max * w + 16);
+}
+
+// Suffix sums -> this thread's F(s) for each s, block-reduced into out[0..s_max) (uint64)
+// and out[kMaxS] (count of nonzero finite elements).  F(s) of one thread is a sum of
+// per-element losses, hence >= 0.
+__device__ __forceinline__ void hist_flush(const LossHist &H, unsigned long long *out) {
+    __shared__ unsigned long long red[kMaxS + 1];
+    if (threadIdx.x <= kMaxS) red[threadIdx.x] = 0;
     __syncthreads();
-#pragma unroll
-    for (int s = 0; s < S_MAX; ++s) {
-        if (s >= s_max) break;
-        unsigned long long v = acc[s];
+    long long C = 0, Y = 0;
+    for (int q = H.s_max; q >= 1; --q) {
+        C += H.cnt[(q - 1) * blockDim.x + threadIdx.x];
+        Y += H.ysum[(q - 1) * blockDim.x + threadIdx.x];
+        unsigned long long v = (unsigned long long)(Y - (long long)q * H.w * C);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[s], v);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(&red[q - 1], v);
     }
-    unsigned long long c = cnt;
+    unsigned long long c = H.nnz;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffff, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&red[S_MAX], c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&red[kMaxS], c);
     __syncthreads();
-    if (threadIdx.x < (unsigned)s_max && red[threadIdx.x]) atomicAdd(&out[threadIdx.x], red[threadIdx.x]);
-    if (threadIdx.x == 0 && red[S_MAX]) atomicAdd(&out[kMaxS], red[S_MAX]);
+    if (threadIdx.x < (unsigned)H.s_max && red[threadIdx.x])
+        atomicAdd(&out[threadIdx.x], red[threadIdx.x]);
+    if (threadIdx.x == 0 && red[kMaxS]) atomicAdd(&out[kMaxS], red[kMaxS]);
 }
 
-// Contiguous vectors: one 256-thread block per vector; pass 1 exponent, pass 2 losses.
+// Contiguous vectors: persistent 256-thread blocks, one vector at a time (pass 1 its
+// exponent, pass 2 the histogram; the second read hits L2); one flush per block.
 __global__ void __launch_bounds__(256) k_loss_contig(const double *__restrict__ M, int64_t ld,
                                                      int64_t rows, int64_t kdim, int w, int s_max,
                                                      unsigned long long *__restrict__ out) {
     __shared__ int32_t kred[8];
-    const int64_t r = blockIdx.x;
-    const double *v = M + r * ld;
-    int32_t key = kKeyEmpty;
-    for (int64_t l = threadIdx.x; l < kdim; l += 256) key = max(key, exp_key_a(__ldg(v + l)));
+    LossHist H = hist_init(w, s_max);
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const double *v = M + r * ld;
+        int32_t key = kKeyEmpty;
+        int64_t l = threadIdx.x;
+        for (; l + 3 * 256 < kdim; l += 4 * 256) {
+            double x[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
-    if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = key;
-    __syncthreads();
-    key = kred[0];
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
 #pragma unroll
-    for (int i = 1; i < 8; ++i) key = max(key, kred[i]);
-    uint32_t acc[kMaxS];
+            for (int i = 0; i < 4; ++i) key = max(key, exp_key_a(x[i]));
+        }
+        for (; l < kdim; l += 256) key = max(key, exp_key_a(__ldg(v + l)));
 #pragma unroll
-    for (int s = 0; s < kMaxS; ++s) acc[s] = 0;
-    uint32_t cnt = 0;
-    if (key != kExpNonFinite && key != kKeyEmpty) {  // non-finite / zero vectors: no loss
-        for (int64_t l = threadIdx.x; l < kdim; l += 256) add_loss<kMaxS>(__ldg(v + l), key, w, s_max, acc, cnt);
+        for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
+        if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = key;
+        __syncthreads();
+        key = kred[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) key = max(key, kred[i]);
+        __syncthreads();  // kred is rewritten for the next vector
+        if (key == kExpNonFinite || key == kKeyEmpty) continue;  // non-finite / zero: no loss
+        l = threadIdx.x;
+        for (; l + 3 * 256 < kdim; l += 4 * 256) {
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) H.add(x[i], key);
+        }
+        for (; l < kdim; l += 256) H.add(__ldg(v + l), key);
     }
-    flush<kMaxS>(acc, cnt, s_max, out);
+    hist_flush(H, out);
 }
 
 // Strided vectors (element l of vector r at M[r + l ld]; complex: the (re, im) pair at
 // 2 (r + l ld)): one thread per vector and a slice of l per blockIdx.y; the exponent comes
-// from keys.
+// from keys (launch_expscan).
 template <int CPX>
 __global__ void __launch_bounds__(256) k_loss_strided(const double *__restrict__ M, int64_t ld,
                                                       int64_t rows, int64_t kdim, int64_t lchunk,
                                                       const int32_t *__restrict__ keys, int w,
                                                       int s_max, unsigned long long *__restrict__ out) {
+    LossHist H = hist_init(w, s_max);
     const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-    uint32_t acc[kMaxS];
+    const int32_t key = r < rows ? keys[r] : kKeyEmpty;
+    if (key != kExpNonFinite && key != kKeyEmpty) {
+        const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
+        const int64_t l1 = min(kdim, l0 + lchunk);
+        int64_t l = l0;
+        if (CPX) {
+            const double2 *Mc = reinterpret_cast<const double2 *>(M);
+            for (; l + 4 <= l1; l += 4) {
+                double2 z[4];
 #pragma unroll
-    for (int s = 0; s < kMaxS; ++s) acc[s] = 0;
-    uint32_t cnt = 0;
-    if (r < rows) {
-        const int32_t key = keys[r];
-        if (key != kExpNonFinite && key != kKeyEmpty) {
-            const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
-            const int64_t l1 = min(kdim, l0 + lchunk);
-            for (int64_t l = l0; l < l1; ++l) {
-                if (CPX) {
-                    const double2 z = __ldg(reinterpret_cast<const double2 *>(M) + r + l * ld);
-                    add_loss<kMaxS>(z.x, key, w, s_max, acc, cnt);
-                    add_loss<kMaxS>(z.y, key, w, s_max, acc, cnt);
-                } else {
-                    add_loss<kMaxS>(__ldg(M + r + l * ld), key, w, s_max, acc, cnt);
+                for (int i = 0; i < 4; ++i) z[i] = __ldg(Mc + r + (l + i) * ld);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    H.add(z[i].x, key);
+                    H.add(z[i].y, key);
                 }
             }
-        }
-    }
-    flush<kMaxS>(acc, cnt, s_max, out);
-}
-
-template <int CPX>
-__global__ void k_expscan_strided_a(const double *__restrict__ M, int64_t ld, int64_t rows,
-                                    int64_t kdim, int64_t lchunk, int32_t *__restrict__ keys) {
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
-    if (r >= rows) return;
-    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
-    const int64_t l1 = min(kdim, l0 + lchunk);
-    int32_t key = kKeyEmpty;
-    for (int64_t l = l0; l < l1; ++l) {
-        if (CPX) {
-            const double2 z = __ldg(reinterpret_cast<const double2 *>(M) + r + l * ld);
-            key = max(key, max(exp_key_a(z.x), exp_key_a(z.y)));
+            for (; l < l1; ++l) {
+                const double2 z = __ldg(Mc + r + l * ld);
+                H.add(z.x, key);
+                H.add(z.y, key);
+            }
         } else {
-            key = max(key, exp_key_a(__ldg(M + r + l * ld)));
+            for (; l + 8 <= l1; l += 8) {
+                double x[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x[i] = __ldg(M + r + (l + i) * ld);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) H.add(x[i], key);
+            }
+            for (; l < l1; ++l) H.add(__ldg(M + r + l * ld), key);
         }
     }
-    if (key != kKeyEmpty) atomicMax(keys + r, key);
+    hist_flush(H, out);
 }
 
 }  // namespace
@@ -172,33 +227,36 @@ cudaError_t launch_mantissa_loss(const double *M, int64_t ld, bool contiguous, i
                                  int32_t *key_scratch, int num_sms, cudaStream_t st,
                                  int *launches, int cpx) {
     if (rows <= 0 || kdim <= 0) return cudaSuccess;
-    if (s_max < 1 || s_max > kMaxS) return cudaErrorInvalidValue;
+    if (s_max < 1 || s_max > kMaxS || w < 1 || w > 7) return cudaErrorInvalidValue;
+    // per-thread bins hold int32 sums of y <= 2^12 over <= 2^18 elements per thread
+    const size_t smem = hist_smem(s_max, 256, w);
+    if (smem > 48 * 1024) {  // s_max > 23: opt in (per device, so on every call; cheap)
+        cudaFuncSetAttribute(k_loss_contig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_loss_strided<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_loss_strided<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
     if (contiguous) {
-        k_loss_contig<<<(unsigned)rows, 256, 0, st>>>(M, ld, rows, kdim, w, s_max, out);
+        if (ceil_div(kdim, 256) > (1 << 18)) return cudaErrorInvalidValue;
+        int64_t blocks = 4 * (int64_t)num_sms;
+        if (blocks > rows) blocks = rows;
+        k_loss_contig<<<(unsigned)blocks, 256, smem, st>>>(M, ld, rows, kdim, w, s_max, out);
         ++*launches;
         return cudaGetLastError();
     }
-    cudaError_t e = cudaMemsetAsync(key_scratch, 0x80, sizeof(int32_t) * rows, st);
+    cudaError_t e = launch_expscan(M, ld, rows, kdim, key_scratch, num_sms, st, launches, cpx);
     if (e != cudaSuccess) return e;
     const int64_t rblocks = ceil_div(rows, 256);
     int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
     if (ysplit < 1) ysplit = 1;
     int64_t lchunk = ceil_div(kdim, ysplit);
     if (lchunk < 64) lchunk = 64;
+    if (lchunk > (1 << 17)) lchunk = 1 << 17;  // (re, im): 2 elements per step
     ysplit = ceil_div(kdim, lchunk);
     if (cpx)
-        k_expscan_strided_a<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-            M, ld, rows, kdim, lchunk, key_scratch);
-    else
-        k_expscan_strided_a<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-            M, ld, rows, kdim, lchunk, key_scratch);
-    ++*launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (cpx)
-        k_loss_strided<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+        k_loss_strided<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, smem, st>>>(
             M, ld, rows, kdim, lchunk, key_scratch, w, s_max, out);
     else
-        k_loss_strided<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+        k_loss_strided<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, smem, st>>>(
             M, ld, rows, kdim, lchunk, key_scratch, w, s_max, out);
     ++*launches;
     return cudaGetLastError();

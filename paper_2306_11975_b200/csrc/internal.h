@@ -39,6 +39,9 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
                          cudaStream_t st, int *launches, int cpx = 0, int conj = 0);
 
+cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t kel, int32_t *keys,
+                           int num_sms, cudaStream_t st, int *launches, int cpx);
+
 // ---- INT8-AUTO mantissa-loss scan (f2) -------------------------------------------------
 cudaError_t launch_mantissa_loss(const double *M, int64_t ld, bool contiguous, int64_t rows,
                                  int64_t kdim, int w, int s_max, unsigned long long *out,

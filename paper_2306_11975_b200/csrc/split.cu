@@ -351,6 +351,33 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
     }
 }
 
+}  // namespace
+
+// Exponent keys of strided vectors (element l of vector r at M[r + l ld]; cpx: (re, im)
+// pairs at 2 (r + l ld), kel counts complex elements): keys[r] = max exp_key over the vector.
+cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t kel, int32_t *keys,
+                           int num_sms, cudaStream_t st, int *launches, int cpx) {
+    cudaError_t e = cudaMemsetAsync(keys, 0x80, sizeof(int32_t) * rows, st);
+    if (e != cudaSuccess) return e;
+    const int64_t rblocks = ceil_div(rows, 256);
+    int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
+    ysplit = ysplit < 1 ? 1 : ysplit;
+    int64_t lchunk = round_up(ceil_div(kel, ysplit), 8);
+    if (lchunk < 64) lchunk = 64;
+    ysplit = ceil_div(kel, lchunk);
+    if (ysplit < 1) ysplit = 1;
+    if (cpx)
+        k_expscan_strided<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+            M, ld, rows, kel, lchunk, keys);
+    else
+        k_expscan_strided<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+            M, ld, rows, kel, lchunk, keys);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+namespace {
+
 template <int W, int S, int CPX>
 cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t rows,
                            int64_t kdim, int64_t k_pad, int s, bool reverse, int conj,
@@ -369,20 +396,9 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
         return cudaGetLastError();
     }
     // strided: exponent scan then transposing slice
-    cudaError_t e = cudaMemsetAsync(key_scratch, 0x80, sizeof(int32_t) * rows, st);
+    cudaError_t e = launch_expscan(M, ld, rows, CPX ? kdim / 2 : kdim, key_scratch, num_sms, st,
+                                   launches, CPX ? 1 : 0);
     if (e != cudaSuccess) return e;
-    const int64_t kel = CPX ? kdim / 2 : kdim;  // elements along the vector
-    const int64_t rblocks = ceil_div(rows, 256);
-    int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
-    ysplit = ysplit < 1 ? 1 : ysplit;
-    int64_t lchunk = round_up(ceil_div(kel, ysplit), 8);
-    if (lchunk < 64) lchunk = 64;
-    ysplit = ceil_div(kel, lchunk);
-    if (ysplit < 1) ysplit = 1;
-    k_expscan_strided<CPX ? 1 : 0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-        M, ld, rows, kel, lchunk, key_scratch);
-    ++*launches;
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_split_strided<W, S, CPX><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(k_pad, 128)),
                                  256, 0, st>>>(M, ld, rows, kdim, k_pad, s, reverse, conj,
                                                key_scratch, planes, plane_stride, E);

@@ -90,3 +90,17 @@ def test_auto_zgemm(h, ta, tb):
     got = dC.cpu().numpy().reshape(n, m).T
     assert np.array_equal(got, ref)
     h.set_auto(0.0, 20)
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "T")])
+def test_auto_wide_range_smax32(h, ta, tb):
+    """Huge exponent spreads (phi = 8) need many slices; s_max = 32 takes the opt-in
+    shared-memory path of the histogram kernels, and T > 0 exercises the F_t - F_l split."""
+    m, n, k = 300, 260, 700
+    A = synth.gen_phi(*_stored(ta, m, k), 8.0, 81)
+    B = synth.gen_phi(*_stored(tb, k, n), 8.0, 82)
+    for T in (0.0, 0.5, 3.0, 20.0):
+        s_ref = O.auto_splits(ta, tb, m, n, k, A, A.shape[0], B, B.shape[0], T, 32)
+        h.set_auto(T, 32)
+        assert h.auto_splits(ta, tb, m, n, k, dev(A), A.shape[0], dev(B), B.shape[0]) == s_ref
+    h.set_auto(0.0, 20)
