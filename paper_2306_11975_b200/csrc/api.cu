@@ -191,21 +191,21 @@ ozimmu_status_t scale_only(ozimmu_handle_t h, int64_t m, int64_t n, double beta,
 // Slice op(A): rows of op(A) are contiguous along k iff transA != N.
 cudaError_t slice_a(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t k, int64_t k_pad,
                     const double *A, int64_t lda, int s, int w, int8_t *planes, int32_t *E,
-                    int32_t *keys, int *launches) {
+                    int32_t *keys, int *launches, BatchMap vm = BatchMap()) {
     const bool contig = transA != OZIMMU_OP_N;
     return launch_split(A, lda, contig, m, k, k_pad, s, w, /*reverse=*/false, planes,
-                        (int64_t)m * k_pad, E, keys, h->num_sms, h->stream, launches);
+                        (int64_t)m * k_pad, E, keys, h->num_sms, h->stream, launches, 0, 0, vm);
 }
 
 // Slice op(B) into a B-slice buffer: columns of op(B) are contiguous along k iff transB == N.
 cudaError_t slice_b(ozimmu_handle_t h, ozimmu_op_t transB, int64_t k, int64_t n, int64_t k_pad,
                     const double *B, int64_t ldb, int s, int w, uint8_t *bbuf, int32_t *keys,
-                    int *launches) {
+                    int *launches, BatchMap vm = BatchMap()) {
     const bool contig = transB == OZIMMU_OP_N;
     int8_t *planes = reinterpret_cast<int8_t *>(bbuf);
     int32_t *E = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
     return launch_split(B, ldb, contig, n, k, k_pad, s, w, /*reverse=*/true, planes,
-                        (int64_t)n * k_pad, E, keys, h->num_sms, h->stream, launches);
+                        (int64_t)n * k_pad, E, keys, h->num_sms, h->stream, launches, 0, 0, vm);
 }
 
 // f2 INT8-AUTO (reading A17): exact per-s mantissa-loss sums of the rows of
@@ -260,8 +260,11 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
                        int s, int w, const int8_t *a_planes, const int32_t *EA,
                        const int8_t *b_planes, const int32_t *EB, int64_t b_plane_rows,
                        double alpha, double beta, double *C, int64_t ldc, int64_t *scratch,
-                       unsigned int *sync, int *launches) {
+                       unsigned int *sync, int *launches, BatchMap crow = BatchMap(),
+                       BatchMap ccol = BatchMap()) {
     GemmArgs ga{};
+    ga.c_rows = crow;
+    ga.c_cols = ccol;
     ga.a_planes = a_planes;
     ga.b_planes = b_planes;
     ga.b_plane_rows = b_plane_rows;
@@ -304,10 +307,14 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
     return cudaSuccess;
 }
 
+// amap / bmap: stacked batches of op(A) rows / op(B) columns; crow / ccol: the matching
+// row / column maps of C (strided-batched calls with a shared operand).
 ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t n, int64_t k,
                           double alpha, const double *A, int64_t lda, const uint8_t *bbuf_ext,
                           ozimmu_op_t transB, const double *B, int64_t ldb, double beta,
-                          double *C, int64_t ldc, int s) {
+                          double *C, int64_t ldc, int s, BatchMap amap = BatchMap(),
+                          BatchMap bmap = BatchMap(), BatchMap crow = BatchMap(),
+                          BatchMap ccol = BatchMap()) {
     const int w = slice_width(k);
     const int64_t k_pad = round_up(k, 16);
     GemmPlan gp;
@@ -326,19 +333,20 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     mark(h, 0);
     if (!bbuf_ext) {
         uint8_t *b = base + L.b_buf;
-        cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, b, keys, &launches);
+        cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, b, keys, &launches, bmap);
         if (e != cudaSuccess) return cuda_status(e);
         bbuf = b;
         slice_bytes += (int64_t)s * n * k_pad + 4 * n;
     }
     mark(h, 1);
-    cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches);
+    cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches,
+                            amap);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 2);
     e = fused_gemm(h, gp, m, n, k_pad, s, w, a_planes, EA, reinterpret_cast<const int8_t *>(bbuf),
                    reinterpret_cast<const int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s)), 0,
                    alpha, beta, C, ldc, reinterpret_cast<int64_t *>(base + L.scratch),
-                   reinterpret_cast<unsigned int *>(base + L.sync), &launches);
+                   reinterpret_cast<unsigned int *>(base + L.sync), &launches, crow, ccol);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 3);
     mark_done(h);
@@ -725,6 +733,82 @@ static size_t zgemm_ws(int64_t m, int64_t n, int64_t k, int s, int num_sms, Gemm
     return L.total;
 }
 
+// ZGEMM after validation / AUTO (reading A16).  amap / bmap: stacked batches of rows of
+// op(A) / columns of op(B) (strides in complex elements); crow / ccol: C maps (complex).
+static ozimmu_status_t zgemm_core(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB,
+                                  int64_t m, int64_t n, int64_t k, const double *alpha,
+                                  const double *A, int64_t lda, const double *B, int64_t ldb,
+                                  const double *beta, double *C, int64_t ldc, int s,
+                                  BatchMap amap = BatchMap(), BatchMap bmap = BatchMap(),
+                                  BatchMap crow = BatchMap(), BatchMap ccol = BatchMap()) {
+    ozimmu_status_t st;
+    const int64_t K2 = 2 * k;
+    const int w = slice_width(K2);
+    const int64_t k_pad = round_up(K2, 16);
+    GemmPlan gp;
+    Layout L;
+    if (!zgemm_ws(m, n, k, s, h->num_sms, &gp, &L)) return OZIMMU_ERR_UNSUPPORTED;
+    void *ws = nullptr;
+    if ((st = get_ws(h, L.total, &ws))) return st;
+    uint8_t *base = static_cast<uint8_t *>(ws);
+    int8_t *a_planes = reinterpret_cast<int8_t *>(base + L.a_planes);
+    int32_t *EA = reinterpret_cast<int32_t *>(base + L.a_exp);
+    uint8_t *bbuf = base + L.b_buf;
+    int8_t *b_planes = reinterpret_cast<int8_t *>(bbuf);
+    int32_t *EB = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(2 * n, k_pad, s));
+    int32_t *keys = reinterpret_cast<int32_t *>(base + L.keys);
+    int launches = 0;
+    mark(h, 0);
+    // columns of op(B): contiguous (re, im) pairs iff transB == N -> 2n plane rows
+    const bool bcontig = transB == OZIMMU_OP_N;
+    // batch strides in the units of the vector ld: doubles (contiguous) or complex (strided)
+    BatchMap bm = bmap;
+    if (bcontig) bm.stride *= 2;
+    cudaError_t e = launch_split(B, bcontig ? 2 * ldb : ldb, bcontig, n, K2, k_pad, s, w,
+                                 /*reverse=*/true, b_planes, 2 * n * k_pad, EB, keys, h->num_sms,
+                                 h->stream, &launches, /*cpx=*/2, transB == OZIMMU_OP_C, bm);
+    if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 1);
+    const bool acontig = transA != OZIMMU_OP_N;
+    BatchMap am = amap;
+    if (acontig) am.stride *= 2;
+    e = launch_split(A, acontig ? 2 * lda : lda, acontig, m, K2, k_pad, s, w, /*reverse=*/false,
+                     a_planes, m * k_pad, EA, keys, h->num_sms, h->stream, &launches, /*cpx=*/1,
+                     transA == OZIMMU_OP_C, am);
+    if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 2);
+    GemmArgs ga{};
+    ga.a_planes = a_planes;
+    ga.b_planes = b_planes;
+    ga.EA = EA;
+    ga.EB = EB;
+    ga.m = m;
+    ga.n = 2 * n;
+    ga.k_pad = k_pad;
+    ga.s = s;
+    ga.w = w;
+    ga.alpha = alpha[0];
+    ga.alpha_im = alpha[1];
+    ga.beta = beta[0];
+    ga.beta_im = beta[1];
+    ga.C = C;
+    ga.ldc = ldc;
+    ga.c_rows = crow;
+    // GEMM columns 2j / 2j+1 are complex column j: the column map acts on j (store_row)
+    ga.c_cols = ccol;
+    ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
+    static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
+    ga.wave_counter = no_sync ? nullptr : reinterpret_cast<unsigned int *>(base + L.sync);
+    e = launch_gemm(ga, gp, EPI_ZGEMM, h->stream, &launches);
+    if (e != cudaSuccess) return cuda_status(e);
+    mark(h, 3);
+    mark_done(h);
+    fill_report(h, s, w, m, n, K2, &gp, launches,
+                (int64_t)s * (m + 2 * n) * k_pad + 4 * (m + 2 * n));
+    h->report.int8_macs = (int64_t)s * (s + 1) / 2 * m * (2 * n) * K2;
+    return OZIMMU_SUCCESS;
+}
+
 size_t ozimmu_zgemm_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m, int64_t n,
                                     int64_t k, int num_slices) {
     if (!valid_op(transA) || !valid_op(transB) || m < 0 || n < 0 || k < 1 || num_slices < 1 ||
@@ -769,69 +853,26 @@ ozimmu_status_t ozimmu_zgemm(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t 
                          /*cpx=*/true);
         if (st) return st;
     }
-    const int s = num_slices;
-    const int64_t K2 = 2 * k;
-    const int w = slice_width(K2);
-    const int64_t k_pad = round_up(K2, 16);
-    GemmPlan gp;
-    Layout L;
-    if (!zgemm_ws(m, n, k, s, h->num_sms, &gp, &L)) return OZIMMU_ERR_UNSUPPORTED;
-    void *ws = nullptr;
-    if ((st = get_ws(h, L.total, &ws))) return st;
-    uint8_t *base = static_cast<uint8_t *>(ws);
-    int8_t *a_planes = reinterpret_cast<int8_t *>(base + L.a_planes);
-    int32_t *EA = reinterpret_cast<int32_t *>(base + L.a_exp);
-    uint8_t *bbuf = base + L.b_buf;
-    int8_t *b_planes = reinterpret_cast<int8_t *>(bbuf);
-    int32_t *EB = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(2 * n, k_pad, s));
-    int32_t *keys = reinterpret_cast<int32_t *>(base + L.keys);
-    int launches = 0;
-    mark(h, 0);
-    // columns of op(B): contiguous (re, im) pairs iff transB == N -> 2n plane rows
-    const bool bcontig = transB == OZIMMU_OP_N;
-    cudaError_t e = launch_split(B, bcontig ? 2 * ldb : ldb, bcontig, n, K2, k_pad, s, w,
-                                 /*reverse=*/true, b_planes, 2 * n * k_pad, EB, keys, h->num_sms,
-                                 h->stream, &launches, /*cpx=*/2, transB == OZIMMU_OP_C);
-    if (e != cudaSuccess) return cuda_status(e);
-    mark(h, 1);
-    const bool acontig = transA != OZIMMU_OP_N;
-    e = launch_split(A, acontig ? 2 * lda : lda, acontig, m, K2, k_pad, s, w, /*reverse=*/false,
-                     a_planes, m * k_pad, EA, keys, h->num_sms, h->stream, &launches, /*cpx=*/1,
-                     transA == OZIMMU_OP_C);
-    if (e != cudaSuccess) return cuda_status(e);
-    mark(h, 2);
-    GemmArgs ga{};
-    ga.a_planes = a_planes;
-    ga.b_planes = b_planes;
-    ga.EA = EA;
-    ga.EB = EB;
-    ga.m = m;
-    ga.n = 2 * n;
-    ga.k_pad = k_pad;
-    ga.s = s;
-    ga.w = w;
-    ga.alpha = alpha[0];
-    ga.alpha_im = alpha[1];
-    ga.beta = beta[0];
-    ga.beta_im = beta[1];
-    ga.C = C;
-    ga.ldc = ldc;
-    ga.chunk_scratch = reinterpret_cast<int64_t *>(base + L.scratch);
-    static const bool no_sync = getenv("OZIMMU_NO_WAVE_SYNC") != nullptr;
-    ga.wave_counter = no_sync ? nullptr : reinterpret_cast<unsigned int *>(base + L.sync);
-    e = launch_gemm(ga, gp, EPI_ZGEMM, h->stream, &launches);
-    if (e != cudaSuccess) return cuda_status(e);
-    mark(h, 3);
-    mark_done(h);
-    fill_report(h, s, w, m, n, K2, &gp, launches,
-                (int64_t)s * (m + 2 * n) * k_pad + 4 * (m + 2 * n));
-    h->report.int8_macs = (int64_t)s * (s + 1) / 2 * m * (2 * n) * K2;
+    st = zgemm_core(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, num_slices);
     h->report.launches += auto_launches;
-    return OZIMMU_SUCCESS;
+    return st;
 }
 
 
 // ---- f3: strided-batched forms (cuBLAS-style), quantum-circuit gate application -----------
+
+// A batch with a shared operand (strideB == 0 or strideA == 0) and a fixed s runs as ONE
+// fused GEMM: the rows of the op(A_b) (shared B) or the columns of the op(B_b) (shared A) are
+// stacked through a BatchMap in the slicing kernels, the shared operand is sliced once, and
+// the epilogue maps stacked rows / columns back to C_b.  Every element sees the operation
+// sequence of the per-item call, so each C_b is bitwise what ozimmu_dgemm returns for it.
+// Other batches (independent A_b and B_b, or INT8-AUTO, where s is chosen per item) loop.
+static bool fuse_batch(int64_t m, int64_t n, int64_t k, int64_t strideA, int64_t strideB,
+                       int64_t batch, int num_slices, bool alpha0) {
+    static const bool off = getenv("OZIMMU_NO_BATCH_FUSE") != nullptr;  // experiments
+    return !off && batch > 1 && num_slices > 0 && (strideA == 0 || strideB == 0) && m > 0 &&
+           n > 0 && k > 0 && !alpha0;
+}
 
 ozimmu_status_t ozimmu_dgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t transA,
                                              ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
@@ -843,33 +884,21 @@ ozimmu_status_t ozimmu_dgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t tran
     if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
     if (batch < 0 || strideA < 0 || strideB < 0 || strideC < 0) return OZIMMU_ERR_INVALID_VALUE;
     if (batch == 0) return OZIMMU_SUCCESS;
-    // shared op(B) (strideB == 0), fixed s, real alpha != 0: slice B once, reuse the buffer
-    const bool share_b = strideB == 0 && batch > 1 && num_slices > 0 && alpha && *alpha != 0.0 &&
-                         m > 0 && n > 0 && k > 0;
-    if (share_b) {
+    if (alpha && fuse_batch(m, n, k, strideA, strideB, batch, num_slices, *alpha == 0.0)) {
         ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc,
                                           num_slices);
         if (st) return st;
-        if (!valid_op(transB) || !B) return OZIMMU_ERR_INVALID_VALUE;
-        if (ldb < ((transB == OZIMMU_OP_N ? k : n) > 1 ? (transB == OZIMMU_OP_N ? k : n) : 1))
-            return OZIMMU_ERR_INVALID_VALUE;
+        const int64_t brows = transB == OZIMMU_OP_N ? k : n;
+        if (!valid_op(transB) || !B || ldb < (brows > 1 ? brows : 1)) return OZIMMU_ERR_INVALID_VALUE;
         if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
-        const size_t bb = ozimmu_b_slices_bytes(n, k, num_slices);
-        void *bbuf = nullptr;
-        if (cudaMallocAsync(&bbuf, bb, h->stream) != cudaSuccess) {
-            cudaGetLastError();
-            return OZIMMU_ERR_WORKSPACE;
-        }
-        st = ozimmu_slice_b(h, transB, k, n, B, ldb, num_slices, bbuf);
-        int launches = h->report.launches;
-        for (int64_t b = 0; b < batch && st == OZIMMU_SUCCESS; ++b) {
-            st = ozimmu_dgemm_presliced_b(h, transA, m, n, k, alpha, A + b * strideA, lda, bbuf,
-                                          beta, C + b * strideC, ldc, num_slices);
-            launches += h->report.launches;
-        }
-        cudaFreeAsync(bbuf, h->stream);
-        h->report.launches = launches;
-        return st;
+        if (strideB == 0)  // shared op(B): stack the rows of op(A_b) and of C_b
+            return gemm_core(h, transA, batch * m, n, k, *alpha, A, lda, nullptr, transB, B, ldb,
+                             *beta, C, ldc, num_slices, BatchMap{m, strideA}, BatchMap(),
+                             BatchMap{m, strideC}, BatchMap());
+        // shared op(A): stack the columns of op(B_b) and of C_b
+        return gemm_core(h, transA, m, batch * n, k, *alpha, A, lda, nullptr, transB, B, ldb,
+                         *beta, C, ldc, num_slices, BatchMap(), BatchMap{n, strideB}, BatchMap(),
+                         BatchMap{n, strideC});
     }
     int launches = 0;
     for (int64_t b = 0; b < batch; ++b) {
@@ -892,6 +921,24 @@ ozimmu_status_t ozimmu_zgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t tran
                                              int num_slices) {
     if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
     if (batch < 0 || strideA < 0 || strideB < 0 || strideC < 0) return OZIMMU_ERR_INVALID_VALUE;
+    if (batch == 0) return OZIMMU_SUCCESS;
+    if (alpha && fuse_batch(m, n, k, strideA, strideB, batch, num_slices,
+                            alpha[0] == 0.0 && alpha[1] == 0.0)) {
+        ozimmu_status_t st = check_common(h, transA, m, n, k, alpha, A, lda, beta, C, ldc,
+                                          num_slices);
+        if (st) return st;
+        const int64_t brows = transB == OZIMMU_OP_N ? k : n;
+        if (!valid_op(transB) || !B || ldb < (brows > 1 ? brows : 1)) return OZIMMU_ERR_INVALID_VALUE;
+        if (2 * k > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+        if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+        if (strideB == 0)
+            return zgemm_core(h, transA, transB, batch * m, n, k, alpha, A, lda, B, ldb, beta, C,
+                              ldc, num_slices, BatchMap{m, strideA}, BatchMap(),
+                              BatchMap{m, strideC}, BatchMap());
+        return zgemm_core(h, transA, transB, m, batch * n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                          num_slices, BatchMap(), BatchMap{n, strideB}, BatchMap(),
+                          BatchMap{n, strideC});
+    }
     int launches = 0;
     for (int64_t b = 0; b < batch; ++b) {  // strides in complex elements
         ozimmu_status_t st = ozimmu_zgemm(h, transA, transB, m, n, k, alpha, A + 2 * b * strideA,

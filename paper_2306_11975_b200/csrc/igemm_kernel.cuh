@@ -32,6 +32,7 @@ struct KParams {
     const int32_t *EA, *EB;
     double *C;
     int64_t ldc;
+    BatchMap c_rows, c_cols;     // stacked batches (C element units)
     void *out;
     int64_t *scratch;
     unsigned int *wave_counter;  // soft grid barrier between tile waves (may be null)
@@ -110,19 +111,32 @@ __device__ __forceinline__ void cmul(double ar, double ai, double xr, double xi,
     zi = __fma_rn(ar, xi, __dmul_rn(ai, xr));
 }
 
+// Offset of row `row` / column `col` of C (in C elements) under a stacked-batch map.
+__device__ __forceinline__ int64_t c_row_off(const BatchMap &b, int64_t row) {
+    if (!b.per_item) return row;
+    const int64_t it = row / b.per_item;
+    return it * b.stride + (row - it * b.per_item);
+}
+__device__ __forceinline__ int64_t c_col_off(const BatchMap &b, int64_t col, int64_t ldc) {
+    if (!b.per_item) return col * ldc;
+    const uint32_t it = static_cast<uint32_t>(col) / static_cast<uint32_t>(b.per_item);
+    return (int64_t)it * b.stride + (col - (int64_t)it * b.per_item) * ldc;
+}
+
 // Final output of one row (this thread) of the tile: real C (reading A8) or complex C.
 template <int NC>
 __device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[NC],
                                           const int32_t *ebt, int32_t ea, int64_t row,
                                           int64_t nb) {
+    const int64_t roff = c_row_off(P.c_rows, row);
     if (P.mode == EPI_DGEMM) {
-        double *crow = P.C + row;
+        double *crow = P.C + roff;
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
             const int64_t col = nb * NC + i;
             if (col >= P.n) break;
             const double X = scale_x(acc[i], ea, ebt[i]);
-            double *cp = crow + col * P.ldc;
+            double *cp = crow + c_col_off(P.c_cols, col, P.ldc);
             *cp = P.beta == 0.0 ? __dmul_rn(P.alpha, X)
                                 : __fma_rn(P.alpha, X, __dmul_rn(P.beta, *cp));
         }
@@ -136,7 +150,7 @@ __device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[
             const double xi = scale_x(acc[i + 1], ea, ebt[i + 1]);
             double tr, ti;
             cmul(P.alpha, P.alpha_im, xr, xi, tr, ti);
-            double2 *cp = reinterpret_cast<double2 *>(P.C) + row + (col >> 1) * P.ldc;
+            double2 *cp = reinterpret_cast<double2 *>(P.C) + roff + c_col_off(P.c_cols, col >> 1, P.ldc);
             if (!beta0) {
                 const double2 c = *cp;
                 double ur, ui;
@@ -630,6 +644,8 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.EB = a.EB;
     P.C = a.C;
     P.ldc = a.ldc;
+    P.c_rows = a.c_rows;
+    P.c_cols = a.c_cols;
     P.out = a.out;
     P.scratch = p.k_chunks > 1 ? a.chunk_scratch : nullptr;
     P.wave_counter = a.wave_counter;

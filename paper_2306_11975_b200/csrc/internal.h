@@ -34,13 +34,24 @@ inline int slice_width(int64_t k) {
 // complex columns of op(B), each emitting two plane rows 2r = (Re, -Im, ..) and
 // 2r+1 = (Im, Re, ..).  For strided complex vectors `ld` is in complex elements; for
 // contiguous ones it is in doubles.
+// Batched operands stacked into one GEMM (strided-batched calls with a shared operand):
+// vector r of the stacked operand is vector (r % per_item) of item r / per_item, whose
+// data start at item_stride * (r / per_item) (same units as the vector's ld).
+// per_item = 0: no batching.
+struct BatchMap {
+    int64_t per_item = 0;
+    int64_t stride = 0;
+};
+
 cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
                          int64_t k_pad, int s, int w, bool reverse, int8_t *planes,
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
-                         cudaStream_t st, int *launches, int cpx = 0, int conj = 0);
+                         cudaStream_t st, int *launches, int cpx = 0, int conj = 0,
+                         BatchMap vm = BatchMap());
 
 cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t kel, int32_t *keys,
-                           int num_sms, cudaStream_t st, int *launches, int cpx);
+                           int num_sms, cudaStream_t st, int *launches, int cpx,
+                           BatchMap vm = BatchMap());
 
 // ---- INT8-AUTO mantissa-loss scan (f2) -------------------------------------------------
 cudaError_t launch_mantissa_loss(const double *M, int64_t ld, bool contiguous, int64_t rows,
@@ -55,6 +66,8 @@ struct GemmArgs {
     const int8_t *a_planes;  // [s][m][k_pad], natural slice order
     const int8_t *b_planes;  // [s][n][k_pad], REVERSED slice order (index s - q)
     int64_t b_plane_rows;    // rows per B plane in memory (0 = n): column chunk of a larger buffer
+    BatchMap c_rows, c_cols; // stacked batches: row r / column j of C -> item and its offset
+                             // (stride in elements of C: doubles, or complex for EPI_ZGEMM)
     const int32_t *EA, *EB;  // exponents (EPI_DGEMM only)
     int64_t m, n, k_pad;
     int s, w;

@@ -38,6 +38,15 @@ __device__ __forceinline__ int32_t key_to_exp(int32_t key) {
     return key == kKeyEmpty ? 0 : key;  // all-zero vector: E = 0 (reading A11)
 }
 
+// Start of vector r (units of ld): contiguous vectors r * ld, strided vectors r, or the
+// stacked-batch mapping (BatchMap) of either.
+__device__ __forceinline__ int64_t vec_off(int64_t r, int64_t ld, int64_t per_item,
+                                           int64_t item_stride) {
+    if (!per_item) return r * ld;
+    const int64_t b = r / per_item;
+    return b * item_stride + (r - b * per_item) * ld;
+}
+
 // floor(M * 2^sh) mod 2^32 for any integer sh (M < 2^53).
 __device__ __forceinline__ uint32_t shifted_limb(uint64_t M, int sh) {
     uint64_t v;
@@ -165,14 +174,15 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
                                                       int64_t rows, int64_t kdim, int64_t k_pad,
                                                       int s, int reverse, int conj,
                                                       int8_t *__restrict__ planes,
-                                                      int64_t plane_stride, int32_t *__restrict__ E) {
+                                                      int64_t plane_stride, int32_t *__restrict__ E,
+                                                      int64_t per_item, int64_t item_stride) {
     constexpr int VPB = 256 / TPR;  // vectors per block
     __shared__ int32_t red[256 / 32];
     const int sub = threadIdx.x / TPR;
     const int t = threadIdx.x % TPR;
     const int64_t r = static_cast<int64_t>(blockIdx.x) * VPB + sub;
     const bool active = r < rows;
-    const double *v = M + (active ? r : 0) * ld;
+    const double *v = M + vec_off(active ? r : 0, ld, per_item, item_stride);
     const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
     const int64_t nchunk = k_pad / 8;
 
@@ -228,9 +238,11 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
 template <int CPX>
 __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restrict__ M, int64_t ld,
                                                          int64_t rows, int64_t kdim, int64_t lchunk,
-                                                         int32_t *__restrict__ keys) {
+                                                         int32_t *__restrict__ keys,
+                                                         int64_t per_item, int64_t item_stride) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
     if (r >= rows) return;
+    const int64_t ro = vec_off(r, 1, per_item, item_stride);  // element 0 of vector r
     const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
     const int64_t l1 = min(kdim, l0 + lchunk);
     int32_t key = kKeyEmpty;
@@ -240,12 +252,12 @@ __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restric
         for (; l + 4 <= l1; l += 4) {
             double2 x[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = __ldg(Mc + r + (l + i) * ld);
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(Mc + ro + (l + i) * ld);
 #pragma unroll
             for (int i = 0; i < 4; ++i) key = max(key, max(exp_key(x[i].x), exp_key(x[i].y)));
         }
         for (; l < l1; ++l) {
-            const double2 x = __ldg(Mc + r + l * ld);
+            const double2 x = __ldg(Mc + ro + l * ld);
             key = max(key, max(exp_key(x.x), exp_key(x.y)));
         }
         if (key != kKeyEmpty) atomicMax(keys + r, key);
@@ -253,11 +265,11 @@ __global__ void __launch_bounds__(256) k_expscan_strided(const double *__restric
     for (; l + 8 <= l1; l += 8) {
         double x[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = __ldg(M + r + (l + i) * ld);
+        for (int i = 0; i < 8; ++i) x[i] = __ldg(M + ro + (l + i) * ld);
 #pragma unroll
         for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
     }
-    for (; l < l1; ++l) key = max(key, exp_key(__ldg(M + r + l * ld)));
+    for (; l < l1; ++l) key = max(key, exp_key(__ldg(M + ro + l * ld)));
     if (key != kKeyEmpty) atomicMax(keys + r, key);
     }
 }
@@ -279,7 +291,8 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
                                                        const int32_t *__restrict__ keys,
                                                        int8_t *__restrict__ planes,
                                                        int64_t plane_stride,
-                                                       int32_t *__restrict__ E) {
+                                                       int32_t *__restrict__ E,
+                                                       int64_t per_item, int64_t item_stride) {
     __shared__ __align__(16) double tile[32][128];  // [r][swizzled l]
     __shared__ int32_t exps[32];
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
@@ -305,6 +318,7 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
     {
         const int rr = tid & 31;
         const int64_t r = r0 + rr;
+        const int64_t ro = vec_off(r < rows ? r : 0, 1, per_item, item_stride);
         if (CPX) {
             // kdim counts doubles (2 per complex element); complex element (r, lc) is the
             // 16-byte pair at 2 (r + lc ld)
@@ -314,7 +328,7 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
                 const int lc = (tid >> 5) + 8 * it;  // 0..63
                 const int64_t l = l0 + 2 * lc;
                 double2 x = make_double2(0.0, 0.0);
-                if (r < rows && l < kdim) x = __ldg(Mc + r + (l >> 1) * ld);
+                if (r < rows && l < kdim) x = __ldg(Mc + ro + (l >> 1) * ld);
                 tile[rr][tslot(rr, 2 * lc)] = x.x;
                 tile[rr][tslot(rr, 2 * lc + 1)] = x.y;
             }
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
             for (int it = 0; it < 16; ++it) {
                 const int ll = (tid >> 5) + 8 * it;
                 const int64_t l = l0 + ll;
-                tile[rr][tslot(rr, ll)] = (r < rows && l < kdim) ? __ldg(M + r + l * ld) : 0.0;
+                tile[rr][tslot(rr, ll)] = (r < rows && l < kdim) ? __ldg(M + ro + l * ld) : 0.0;
             }
         }
     }
@@ -356,7 +370,7 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
 // Exponent keys of strided vectors (element l of vector r at M[r + l ld]; cpx: (re, im)
 // pairs at 2 (r + l ld), kel counts complex elements): keys[r] = max exp_key over the vector.
 cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t kel, int32_t *keys,
-                           int num_sms, cudaStream_t st, int *launches, int cpx) {
+                           int num_sms, cudaStream_t st, int *launches, int cpx, BatchMap vm) {
     cudaError_t e = cudaMemsetAsync(keys, 0x80, sizeof(int32_t) * rows, st);
     if (e != cudaSuccess) return e;
     const int64_t rblocks = ceil_div(rows, 256);
@@ -368,10 +382,10 @@ cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t ke
     if (ysplit < 1) ysplit = 1;
     if (cpx)
         k_expscan_strided<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-            M, ld, rows, kel, lchunk, keys);
+            M, ld, rows, kel, lchunk, keys, vm.per_item, vm.stride);
     else
         k_expscan_strided<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-            M, ld, rows, kel, lchunk, keys);
+            M, ld, rows, kel, lchunk, keys, vm.per_item, vm.stride);
     ++*launches;
     return cudaGetLastError();
 }
@@ -382,26 +396,29 @@ template <int W, int S, int CPX>
 cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t rows,
                            int64_t kdim, int64_t k_pad, int s, bool reverse, int conj,
                            int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
-                           int num_sms, cudaStream_t st, int *launches) {
+                           int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
     // kdim / k_pad count doubles of the (embedded) vector: 2 per complex element
     if (contiguous) {
         if (k_pad >= 2048) {
             k_split_contig<256, W, S, CPX><<<(unsigned)rows, 256, 0, st>>>(
-                M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E);
+                M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E, vm.per_item,
+                vm.stride);
         } else {
             k_split_contig<32, W, S, CPX><<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(
-                M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E);
+                M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E, vm.per_item,
+                vm.stride);
         }
         ++*launches;
         return cudaGetLastError();
     }
     // strided: exponent scan then transposing slice
     cudaError_t e = launch_expscan(M, ld, rows, CPX ? kdim / 2 : kdim, key_scratch, num_sms, st,
-                                   launches, CPX ? 1 : 0);
+                                   launches, CPX ? 1 : 0, vm);
     if (e != cudaSuccess) return e;
     k_split_strided<W, S, CPX><<<dim3((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(k_pad, 128)),
                                  256, 0, st>>>(M, ld, rows, kdim, k_pad, s, reverse, conj,
-                                               key_scratch, planes, plane_stride, E);
+                                               key_scratch, planes, plane_stride, E,
+                                               vm.per_item, vm.stride);
     ++*launches;
     return cudaGetLastError();
 }
@@ -410,35 +427,35 @@ template <int W, int CPX>
 cudaError_t launch_split_w(const double *M, int64_t ld, bool contiguous, int64_t rows,
                            int64_t kdim, int64_t k_pad, int s, bool reverse, int conj,
                            int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
-                           int num_sms, cudaStream_t st, int *launches) {
+                           int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
     if (s <= 9)
         return launch_split_t<W, 9, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                          planes, plane_stride, E, key_scratch, num_sms, st,
-                                         launches);
+                                         launches, vm);
     if (s <= 16)
         return launch_split_t<W, 16, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                           planes, plane_stride, E, key_scratch, num_sms, st,
-                                          launches);
+                                          launches, vm);
     return launch_split_t<W, 32, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                       planes, plane_stride, E, key_scratch, num_sms, st,
-                                      launches);
+                                      launches, vm);
 }
 
 template <int CPX>
 cudaError_t launch_split_c(const double *M, int64_t ld, bool contiguous, int64_t rows,
                            int64_t kdim, int64_t k_pad, int s, int w, bool reverse, int conj,
                            int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
-                           int num_sms, cudaStream_t st, int *launches) {
+                           int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
     switch (w) {
     case 7: return launch_split_w<7, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                           planes, plane_stride, E, key_scratch, num_sms, st,
-                                          launches);
+                                          launches, vm);
     case 6: return launch_split_w<6, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                           planes, plane_stride, E, key_scratch, num_sms, st,
-                                          launches);
+                                          launches, vm);
     case 5: return launch_split_w<5, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                           planes, plane_stride, E, key_scratch, num_sms, st,
-                                          launches);
+                                          launches, vm);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -448,16 +465,16 @@ cudaError_t launch_split_c(const double *M, int64_t ld, bool contiguous, int64_t
 cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
                          int64_t k_pad, int s, int w, bool reverse, int8_t *planes,
                          int64_t plane_stride, int32_t *E, int32_t *key_scratch, int num_sms,
-                         cudaStream_t st, int *launches, int cpx, int conj) {
+                         cudaStream_t st, int *launches, int cpx, int conj, BatchMap vm) {
     if (rows <= 0) return cudaSuccess;
     if (s < 1 || s > 32) return cudaErrorInvalidValue;
     switch (cpx) {
     case 0: return launch_split_c<0>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, 0,
-                                     planes, plane_stride, E, key_scratch, num_sms, st, launches);
+                                     planes, plane_stride, E, key_scratch, num_sms, st, launches, vm);
     case 1: return launch_split_c<1>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, conj,
-                                     planes, plane_stride, E, key_scratch, num_sms, st, launches);
+                                     planes, plane_stride, E, key_scratch, num_sms, st, launches, vm);
     case 2: return launch_split_c<2>(M, ld, contiguous, rows, kdim, k_pad, s, w, reverse, conj,
-                                     planes, plane_stride, E, key_scratch, num_sms, st, launches);
+                                     planes, plane_stride, E, key_scratch, num_sms, st, launches, vm);
     default: return cudaErrorInvalidValue;
     }
 }

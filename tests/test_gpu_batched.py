@@ -110,3 +110,72 @@ def test_batched_edge_cases(h):
         h.dgemm_strided_batched("N", "N", 4, 4, 4, 1.0, d, 4, -16, d, 4, 16, 0.0, d, 4, 16, 1, 9)
     with pytest.raises(oz.OzimmuError):
         h.dgemm_strided_batched("N", "N", 4, 4, 4, 1.0, d, 4, 16, d, 4, 16, 0.0, d, 4, 16, -1, 9)
+
+
+def _run_batched_d(h, ta, tb, m, n, k, s, batch, shareA, shareB, alpha, beta, seed):
+    import torch
+    As = [synth.gen_phi(*_stored(ta, m, k), 1.0, seed + (0 if shareA else b)) for b in range(batch)]
+    Bs = [synth.gen_phi(*_stored(tb, k, n), 1.0, seed + 100 + (0 if shareB else b))
+          for b in range(batch)]
+    Cs = [synth.gen_phi(m, n, 1.0, seed + 200 + b) for b in range(batch)]
+    dA = torch.from_numpy(_stack(As[:1] if shareA else As)).cuda()
+    dB = torch.from_numpy(_stack(Bs[:1] if shareB else Bs)).cuda()
+    dC = torch.from_numpy(_stack(Cs)).cuda()
+    h.dgemm_strided_batched(ta, tb, m, n, k, alpha, dA, As[0].shape[0], 0 if shareA else As[0].size,
+                            dB, Bs[0].shape[0], 0 if shareB else Bs[0].size, beta, dC, m, m * n,
+                            batch, s)
+    torch.cuda.synchronize()
+    rep = h.report()
+    got = dC.cpu().numpy()
+    for b in range(batch):
+        ref = O.dgemm(ta, tb, m, n, k, alpha, As[b], As[b].shape[0], Bs[b], Bs[b].shape[0], beta,
+                      Cs[b], m, s)
+        assert np.array_equal(np.asfortranarray(got[b * m * n:(b + 1) * m * n].reshape(n, m).T),
+                              ref), b
+    return rep
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "T"), ("T", "N"), ("N", "T")])
+@pytest.mark.parametrize("share", ["A", "B", "AB"])
+def test_fused_batch_bitexact(h, ta, tb, share):
+    """Shared-operand batches run as one fused GEMM (<= 5 launches) and stay bit-exact per
+    item; m = 16 puts 8 items in one 128-row tile, n = 20 splits items across column tiles."""
+    rep = _run_batched_d(h, ta, tb, 16, 20, 96, 8, 37, "A" in share, "B" in share, 1.25, -0.5,
+                         300)
+    assert rep["launches"] <= 5, rep  # 2 slicing kernels per strided operand + GEMM
+
+
+def test_fused_batch_large_items(h):
+    rep = _run_batched_d(h, "N", "N", 200, 150, 300, 9, 3, False, True, 1.0, 0.0, 400)
+    assert rep["launches"] <= 5
+    rep = _run_batched_d(h, "N", "N", 150, 200, 300, 9, 3, True, False, 1.0, 0.0, 500)
+    assert rep["launches"] <= 5
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("C", "T"), ("T", "C")])
+@pytest.mark.parametrize("share", ["A", "B"])
+def test_fused_batch_zgemm_bitexact(h, ta, tb, share):
+    """Quantum gate application: one 2^d x 2^d gate shared by 2^(N-d-o) state blocks."""
+    import torch
+    m, n, k, s, batch = 16, 24, 64, 12, 9
+    shareA, shareB = share == "A", share == "B"
+    As = [synth.gen_phi_complex(*_stored(ta, m, k), 0.5, 600 + (0 if shareA else b))
+          for b in range(batch)]
+    Bs = [synth.gen_phi_complex(*_stored(tb, k, n), 0.5, 700 + (0 if shareB else b))
+          for b in range(batch)]
+    Cs = [synth.gen_phi_complex(m, n, 0.5, 800 + b) for b in range(batch)]
+    dA = torch.from_numpy(_stack(As[:1] if shareA else As)).cuda()
+    dB = torch.from_numpy(_stack(Bs[:1] if shareB else Bs)).cuda()
+    dC = torch.from_numpy(_stack(Cs)).cuda()
+    alpha, beta = 0.5 + 1.0j, -1.0 + 0.25j
+    h.zgemm_strided_batched(ta, tb, m, n, k, alpha, dA, As[0].shape[0], 0 if shareA else As[0].size,
+                            dB, Bs[0].shape[0], 0 if shareB else Bs[0].size, beta, dC, m, m * n,
+                            batch, s)
+    torch.cuda.synchronize()
+    assert h.report()["launches"] <= 5
+    got = dC.cpu().numpy()
+    for b in range(batch):
+        ref = O.zgemm(ta, tb, m, n, k, alpha, As[b], As[b].shape[0], Bs[b], Bs[b].shape[0], beta,
+                      Cs[b], m, s)
+        assert np.array_equal(np.asfortranarray(got[b * m * n:(b + 1) * m * n].reshape(n, m).T),
+                              ref), b
