@@ -37,6 +37,13 @@ WORKLOADS = {
     "C5": dict(m=2 ** 16, n=2 ** 12, k=2 ** 12, phi=0.1, s=12, seeds=(501, 502), complex=True,
                desc="C5: ZGEMM matmul-(2^16, 2^12, 2^12) = one 12-qubit Haar gate on a 28-qubit "
                     "state vector, s=12"),
+    # the same gate on qubits o..o+d-1 of the middle of the register (o = 4): the state is a
+    # (2^(N-d-o), 2^d, 2^o) tensor and the gate a strided-batched ZGEMM with a shared U:
+    # batch 2^12 of matmul-(2^o, 2^d, 2^d) (column-major view), one fused GEMM here
+    "C5B": dict(m=2 ** 4, n=2 ** 12, k=2 ** 12, batch=2 ** 12, phi=0.1, s=12, seeds=(511, 512),
+                complex=True,
+                desc="C5B: batched ZGEMM, 12-qubit Haar gate on qubits 4..15 of a 28-qubit state: "
+                     "batch 4096 x matmul-(16, 4096, 4096) with shared U, s=12"),
 }
 METRIC = "effective DGEMM TFLOP/s (2mnk/t) vs cuBLAS DGEMM at 1/2/4/8 B200; max rel err"
 INT8_PEAK_NOTE = ("INT8 dense peak = 2 x measured bf16 cuBLAS (nominal 4.5/2.25 POPS ratio); "
@@ -190,7 +197,7 @@ def run_reference(args, wl):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "i8", "data": "synthetic",
-            "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "phi": wl["phi"],
+            "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "batch": batch, "phi": wl["phi"],
                        "parallelism": "cpu oracle, OpenMP"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
@@ -205,19 +212,29 @@ def run_zgemm(args, wl):
 
     import paper_2306_11975_b200 as oz
     m, n, k, s = wl["m"], wl["n"], wl["k"], wl["s"]
+    batch = wl.get("batch", 1)
     torch.cuda.set_device(0)
-    psi = synth.gen_phi_complex(m, k, wl["phi"], wl["seeds"][0])
+    psi = synth.gen_phi_complex(m * batch, k, wl["phi"], wl["seeds"][0])
     psi /= np.linalg.norm(psi)
     U = synth.haar_unitary(k, wl["seeds"][1])
-    dA = torch.from_numpy(np.ascontiguousarray(psi.ravel(order="F"))).cuda()
-    dB = torch.from_numpy(np.ascontiguousarray(U.ravel(order="F"))).cuda()
-    dC = torch.empty(m * n, dtype=torch.complex128, device="cuda")
+    if batch > 1:  # state as (2^(N-d-o), 2^d, 2^o): item b = 2^o x 2^d block, column-major
+        dA = torch.from_numpy(np.ascontiguousarray(psi.ravel(order="C"))).cuda()
+        dB = torch.from_numpy(np.ascontiguousarray(U.ravel(order="C"))).cuda()  # = U^T col-major
+    else:
+        dA = torch.from_numpy(np.ascontiguousarray(psi.ravel(order="F"))).cuda()
+        dB = torch.from_numpy(np.ascontiguousarray(U.ravel(order="F"))).cuda()
+    del psi
+    dC = torch.empty(m * n * batch, dtype=torch.complex128, device="cuda")
     h = oz.Handle(0)
     stream = torch.cuda.current_stream()
     h.set_stream(stream)
 
     def step():
-        h.zgemm("N", "T", m, n, k, 1.0, dA, m, dB, n, 0.0, dC, m, s)
+        if batch > 1:  # C_b = A_b U^T: A_b 2^o x 2^d (ld 2^o), shared op(B) = U^T
+            h.zgemm_strided_batched("N", "N", m, n, k, 1.0, dA, m, m * k, dB, k, 0, 0.0, dC, m,
+                                    m * n, batch, s)
+        else:
+            h.zgemm("N", "T", m, n, k, 1.0, dA, m, dB, n, 0.0, dC, m, s)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -235,22 +252,29 @@ def run_zgemm(args, wl):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     phases = h.timing_read(args.steps + 1)
-    flops = 8.0 * m * n * k
+    flops = 8.0 * m * n * k * batch
     value = flops / (ms / 1e3) / 1e12
     gemm_ms = float(np.mean([p["gemm_ms"] for p in phases]))
     peaks, src = load_peaks()
     int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    ops = float(s * (s + 1)) * m * (2 * n) * (2 * k)
+    ops = float(s * (s + 1)) * m * batch * (2 * n) * (2 * k)
     achieved = ops / (gemm_ms / 1e3) / 1e12
-    Am = dA.view(k, m).t()
-    Bm = dB.view(k, n)  # U stored column-major = U^T row-major; op(B) = U^T
-    Cm = torch.empty(m, n, dtype=torch.complex128, device="cuda")
+    if batch > 1:  # torch: out = U @ X, X = state as (batch, 2^d, 2^o) row-major (bmm)
+        Um = dB.view(k, n)
+        Xm = dA.view(batch, k, m)
+        Cm = torch.empty(batch, n, m, dtype=torch.complex128, device="cuda")
+        cub = lambda: torch.matmul(Um, Xm, out=Cm)  # noqa: E731
+    else:
+        Am = dA.view(k, m).t()
+        Bm = dB.view(k, n)  # U stored column-major = U^T row-major; op(B) = U^T
+        Cm = torch.empty(m, n, dtype=torch.complex128, device="cuda")
+        cub = lambda: torch.matmul(Am, Bm, out=Cm)  # noqa: E731
     for _ in range(2):
-        torch.matmul(Am, Bm, out=Cm)
+        cub()
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(max(3, args.steps // 2)):
-        torch.matmul(Am, Bm, out=Cm)
+        cub()
     e1.record(stream)
     torch.cuda.synchronize()
     cms = e0.elapsed_time(e1) / max(3, args.steps // 2)
@@ -267,7 +291,9 @@ def run_zgemm(args, wl):
                          "unit": "TFLOP/s", "frac": achieved / int8_peak, "traffic": None,
                          "gemm_ms": gemm_ms, "peak_source": src},
             "cublas_zgemm": {"value": cv, "unit": "TFLOP/s", "ms_per_step": cms,
-                             "speedup_ozimmu_vs_cublas": value / cv},
+                             "speedup_ozimmu_vs_cublas": value / cv,
+                             "call": "torch.matmul complex128 (cuBLAS ZGEMM%s)" %
+                                     (" strided-batched, shared U" if batch > 1 else "")},
             "clocks": clk, "gpu_launches": rep["launches"] * args.steps}
     print(json.dumps(line), flush=True)
     h.close()
