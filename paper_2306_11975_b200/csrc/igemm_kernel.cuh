@@ -23,6 +23,10 @@ struct KParams {
     int64_t num_k_blocks, chunk_blocks;
     int k_chunks;
     int64_t tiles_m, tiles_n, num_tiles;
+    // work units: cl = 1 -> one tile per unit; cl = 2 -> a cluster of two CTAs takes the
+    // column tiles (2 j, 2 j + 1) of one row block, the A tiles multicast to both
+    int cl;
+    int64_t units_n, num_units;
     int a_stages, b_stages;
     uint32_t a_stage_bytes, b_stage_bytes;
     uint32_t tmem_cols;
@@ -55,16 +59,17 @@ enum : int { ST_TOTAL = 0, ST_MMA_WAIT_B, ST_MMA_WAIT_A, ST_MMA_WAIT_TMEM, ST_PR
              ST_PROD_WAIT_A, ST_PROD_WAIT_B, ST_EPI_BUSY, ST_EPI_TMEM, ST_EPI_STORE,
              ST_MMA_FIRST_A, ST_MMA_B_TILE0, kStatSlots = 12 };
 
-__device__ __forceinline__ void tile_coords(int64_t t, const KParams &P, int64_t &mb,
-                                            int64_t &nb) {
-    const int64_t per_group = (int64_t)kGroupM * P.tiles_n;
-    const int64_t g = t / per_group;
-    const int64_t r = t % per_group;
+// Grouped raster over units (kGroupM row blocks per group); rank = CTA rank in the cluster.
+__device__ __forceinline__ void tile_coords(int64_t u, const KParams &P, uint32_t rank,
+                                            int64_t &mb, int64_t &nb) {
+    const int64_t per_group = (int64_t)kGroupM * P.units_n;
+    const int64_t g = u / per_group;
+    const int64_t r = u % per_group;
     const int64_t gm0 = g * kGroupM;
     int64_t gsz = P.tiles_m - gm0;
     gsz = gsz < kGroupM ? gsz : kGroupM;
     mb = gm0 + r % gsz;
-    nb = r / gsz;
+    nb = (r / gsz) * P.cl + rank;  // cl = 2: nb may reach tiles_n (a dummy tile, no stores)
 }
 
 // 2^e as a double for e in the normal range (exact).
@@ -188,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     constexpr int s = S;
+    const uint32_t rank = P.cl == 2 ? ptx::cluster_ctarank() : 0u;
 
     if (warp == 5 && lane == 0) {
         for (int i = 0; i < P.b_stages; ++i) {
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < P.a_stages; ++i) {
             ptx::mbar_init(&a_full[i], 1);
-            ptx::mbar_init(&a_empty[i], 1);
+            ptx::mbar_init(&a_empty[i], (uint32_t)P.cl);  // released by both CTAs' MMAs
         }
         ptx::mbar_init(tmem_full, 1);
         ptx::mbar_init(tmem_empty, 4 * 32);
@@ -213,7 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_relinquish();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if (P.cl == 2) ptx::cluster_sync();  // peers' barriers initialised before any multicast
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -234,9 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int z = 0; z < S; z += kPfS)
                     ptx::tma_prefetch_l2_3d(&tmApf, kc, (int32_t)(mb * kBlockM), z);
             };
-            for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x, ++wave) {
+            for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl, ++wave) {
                 int64_t mb, nb;
-                tile_coords(t, P, mb, nb);
+                tile_coords(u, P, rank, mb, nb);
                 long long c0 = P.stats ? clock64() : 0;
                 wave_sync(P, wave);
                 if (P.stats) st_w += clock64() - c0;
@@ -259,11 +266,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_wait(&a_empty[as], aph ^ 1);
                         if (P.stats) st_pa += clock64() - c2;
                         ptx::mbar_arrive_expect_tx(&a_full[as], a_tx);
-                        ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
-                                         (int32_t)(kb * kKB), (int32_t)(mb * kBlockM),
-                                         i, ptx::kEvictNormal);
+                        if (P.cl == 2)  // this CTA's half of the rows, to both CTAs
+                            ptx::tma_load_3d_mc(&tmA, &a_full[as],
+                                                smA + (size_t)as * P.a_stage_bytes +
+                                                    rank * (kBlockM / 2) * kKB,
+                                                (int32_t)(kb * kKB),
+                                                (int32_t)(mb * kBlockM + rank * (kBlockM / 2)), i,
+                                                (uint16_t)0x3, ptx::kEvictNormal);
+                        else
+                            ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
+                                             (int32_t)(kb * kKB), (int32_t)(mb * kBlockM),
+                                             i, ptx::kEvictNormal);
                         if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
+                }
+            }
+            if (P.cl == 2) {
+                // drain: every A slot released by both CTAs, so no multicast arrive is still
+                // in flight towards this CTA when the cluster exits
+                for (int i = 0; i < P.a_stages; ++i) {
+                    ptx::mbar_wait(&a_empty[as], aph ^ 1);
+                    if (++as == P.a_stages) { as = 0; aph ^= 1; }
                 }
             }
             if (P.stats) {
@@ -328,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
 
-        for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+        for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl) {
             for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
                 const int64_t kb0 = (int64_t)c * P.chunk_blocks;
                 int64_t kb1 = kb0 + P.chunk_blocks;
@@ -364,7 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     issue(p, adesc0 + (uint64_t)(ks * 2),
                                           bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4),
                                           ks == 0, x);
-                                ptx::mma_commit(&a_empty[as]);
+                                if (P.cl == 2) ptx::mma_commit_mc(&a_empty[as], (uint16_t)0x3);
+                                else ptx::mma_commit(&a_empty[as]);
                             }
                             __syncwarp();
                             if (++as == P.a_stages) { as = 0; aph ^= 1; }
@@ -385,7 +409,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     issue(p, adesc0 + (uint64_t)(ks * 2),
                                           bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4),
                                           false, 0);
-                                ptx::mma_commit(&a_empty[as]);
+                                if (P.cl == 2) ptx::mma_commit_mc(&a_empty[as], (uint16_t)0x3);
+                                else ptx::mma_commit(&a_empty[as]);
                             }
                             __syncwarp();
                             if (++as == P.a_stages) { as = 0; aph ^= 1; }
@@ -423,9 +448,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kCH = NC < 32 ? NC : 32;  // columns per TMEM read batch
         uint32_t acc_iter = 0, tile_iter = 0;
         long long st_e = 0, st_et = 0, st_es = 0;
-        for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+        for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl) {
             int64_t mb, nb;
-            tile_coords(t, P, mb, nb);
+            tile_coords(u, P, rank, mb, nb);
             const int64_t row = mb * kBlockM + row_local;
             const bool row_ok = row < P.m;
             const bool fp_out = P.mode == EPI_DGEMM || P.mode == EPI_ZGEMM;
@@ -560,7 +585,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             P.stats[(int64_t)blockIdx.x * kStatSlots + ST_EPI_STORE] = st_es;
         }
     }
-    __syncthreads();
+    if (P.cl == 2) ptx::cluster_sync();
+    else __syncthreads();
     if (warp == 0) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem_base, P.tmem_cols);
@@ -611,8 +637,52 @@ inline bool make_map(CUtensorMap *map, const int8_t *base, int64_t k_pad, int64_
 template <int S>
 cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st) {
     constexpr int NC = nc_for(S);
+    auto kern = k_oz_gemm<S>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    // Optional CTA pairs (clusters of 2) sharing the A tiles by TMA multicast (half the A
+    // bytes per SM from L2), OZIMMU_CLUSTER=2.  Off by default: measured 8% slower at
+    // 16384^3, s = 9 (the pair runs in lockstep; the A-ring waits are not L2-bandwidth
+    // bound -- DESIGN.md section 5).  The grid is sized to the co-resident clusters.
+    static const int cl_env = getenv("OZIMMU_CLUSTER") ? atoi(getenv("OZIMMU_CLUSTER")) : 1;
+    const int64_t tiles_m = ceil_div(a.m, kBlockM), tiles_n = ceil_div(a.n, NC);
+    int cl = (cl_env == 2 && tiles_n >= 2 && p.grid >= 2) ? 2 : 1;
+    int grid = p.grid;
+    cudaLaunchAttribute attr[1];
+    if (cl == 2) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        static int maxc_cache[64][33];
+        int &maxc = maxc_cache[dev & 63][S];
+        if (maxc == 0) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((unsigned)(p.grid & ~1));
+            q.blockDim = dim3(kThreads);
+            q.dynamicSmemBytes = p.smem_bytes;
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            q.attrs = attr;
+            q.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&maxc, kern, &q) != cudaSuccess || maxc < 1) {
+                cudaGetLastError();
+                maxc = -1;
+            }
+        }
+        const int64_t units = tiles_m * ceil_div(tiles_n, 2);
+        if (maxc < 1) {
+            cl = 1;
+        } else {
+            int64_t c = maxc < p.grid / 2 ? maxc : p.grid / 2;
+            c = c < units ? c : units;
+            grid = (int)(2 * c);
+        }
+    }
     CUtensorMap tmA, tmB;
-    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, kBlockM, 1)) return cudaErrorInvalidValue;
+    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, cl == 2 ? kBlockM / 2 : kBlockM, 1))
+        return cudaErrorInvalidValue;
     if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s, a.b_plane_rows))
         return cudaErrorInvalidValue;
     CUtensorMap tmApf;  // up to 8 A-slice tiles of a k-block per box (L2 prefetch only)
@@ -655,17 +725,30 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.T = p.T;
     P.region_col[0] = 0;
     P.region_col[1] = (uint32_t)(S * NC);
-    P.full_waves = P.num_tiles / p.grid;
+    P.cl = cl;
+    P.units_n = cl == 2 ? ceil_div(P.tiles_n, 2) : P.tiles_n;
+    P.num_units = P.tiles_m * P.units_n;
+    P.full_waves = P.num_units / (grid / cl);
     if (P.wave_counter) {
-        cudaError_t e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
+        e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
         if (e != cudaSuccess) return e;
     }
-    auto kern = k_oz_gemm<S>;
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
-    if (e != cudaSuccess) return e;
-    kern<<<p.grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, tmApf, P);
-    return cudaGetLastError();
+    if (cl == 1) {
+        kern<<<grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, tmApf, P);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = p.smem_bytes;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmApf, P);
 }
 
 }  // namespace gemm_detail
