@@ -14,8 +14,12 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libozimmu.so")
+# development variants: OZIMMU_VARIANT=<name> OZIMMU_EXTRA_FLAGS="-D..." builds
+# variants/libozimmu_<name>.so (selected at run time with OZIMMU_LIB=...); default: the product
+VARIANT = os.environ.get("OZIMMU_VARIANT", "")
+OBJ = os.path.join(HERE, "build" + ("_" + VARIANT if VARIANT else ""))
+LIB = (os.path.join(HERE, "variants", f"libozimmu_{VARIANT}.so") if VARIANT
+       else os.path.join(HERE, "libozimmu.so"))
 SHIM = os.path.join(HERE, "libozimmu_cublas_shim.so")
 SHIM_SRC = os.path.join(CSRC, "shim", "cublas_shim.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -23,7 +27,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-DOZIMMU_BUILD", "-I", INCLUDE]
+         "-DOZIMMU_BUILD", "-I", INCLUDE] + os.environ.get("OZIMMU_EXTRA_FLAGS", "").split()
 
 
 def sources():
@@ -48,6 +52,7 @@ def _stale(target, deps):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdrs = headers() + [os.path.abspath(__file__)]
     jobs = [s for s in sources() if force or _stale(_obj(s), [s] + hdrs)]
 
@@ -66,6 +71,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if force or jobs or _stale(LIB, objs):
         subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB]
                        + objs, check=True)
+    if VARIANT:
+        return LIB
     # f3: LD_PRELOAD cuBLAS shim (host C++ only; resolves libozimmu.so next to itself)
     if force or _stale(SHIM, [SHIM_SRC, LIB] + hdrs):
         subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-fvisibility=hidden",

@@ -12,7 +12,7 @@
 namespace ozimmu {
 namespace gemm_detail {
 
-constexpr int kThreads = 192;  // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int kThreads = 224;  // warps 0-3 epilogue, 4 TMA producer, 5 and 6 MMA issuers
 constexpr int kBlockM = 128;
 constexpr int kKB = 128;       // K bytes per k-block = one 128B swizzle row
 constexpr int kGroupM = 8;     // grouped raster: 8 row-blocks per group
@@ -52,6 +52,17 @@ struct KParams {
 // s * N_c <= 512 TMEM columns.
 __host__ __device__ constexpr int nc_for(int S) {
     return S * 64 <= 512 ? 64 : (S * 48 <= 512 ? 48 : (S * 32 <= 512 ? 32 : 16));
+}
+
+// Order in which the s A-slice tiles of a k-block are loaded and consumed: p = 1, s, 2,
+// s-1, ... (long and short windows alternate, so the two MMA issuers get similar work; the
+// ascending order measured the same).  The level sums are exact integers, so the order of
+// the MMAs into TMEM does not change any result.
+#ifndef OZ_SLICE_ORDER
+#define OZ_SLICE_ORDER 1
+#endif
+__host__ __device__ constexpr int slice_p(int S, int i) {
+    return OZ_SLICE_ORDER == 0 ? i + 1 : ((i & 1) == 0 ? i / 2 + 1 : S - i / 2);
 }
 
 // stall-counter slots (development instrumentation, OZIMMU_STATS=1)
@@ -198,13 +209,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 5 && lane == 0) {
         for (int i = 0; i < P.b_stages; ++i) {
             ptx::mbar_init(&b_full[i], 1);
-            ptx::mbar_init(&b_empty[i], 1);
+            ptx::mbar_init(&b_empty[i], 2);  // released by both MMA issuers
         }
         for (int i = 0; i < P.a_stages; ++i) {
             ptx::mbar_init(&a_full[i], 1);
             ptx::mbar_init(&a_empty[i], (uint32_t)P.cl);  // released by both CTAs' MMAs
         }
-        ptx::mbar_init(tmem_full, 1);
+        ptx::mbar_init(tmem_full, 2);  // committed by both MMA issuers
         ptx::mbar_init(tmem_empty, 4 * 32);
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
@@ -271,12 +282,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 smA + (size_t)as * P.a_stage_bytes +
                                                     rank * (kBlockM / 2) * kKB,
                                                 (int32_t)(kb * kKB),
-                                                (int32_t)(mb * kBlockM + rank * (kBlockM / 2)), i,
+                                                (int32_t)(mb * kBlockM + rank * (kBlockM / 2)),
+                                                slice_p(S, i) - 1,
                                                 (uint16_t)0x3, ptx::kEvictNormal);
                         else
                             ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
                                              (int32_t)(kb * kKB), (int32_t)(mb * kBlockM),
-                                             i, ptx::kEvictNormal);
+                                             slice_p(S, i) - 1, ptx::kEvictNormal);
                         if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
                 }
@@ -296,58 +308,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 st[ST_PROD_WAIT_B] = st_pb;
             }
         }
-    } else if (warp == 5) {
-        // ===================== MMA issuer =====================
+    } else if (warp == 5 || warp == 6) {
+        // ===================== MMA issuers (two warps) =====================
+        // The A-slice tiles of the ring alternate between warps 5 and 6 (tile t -> warp
+        // 5 + (t & 1)): while one warp waits on its tile's mbarrier and builds descriptors,
+        // the other's MMAs keep the tensor pipe fed (one issuer leaves ~15% of the pipe idle
+        // on the per-tile wait latency; tools/issue_bench.cu).  Every MMA accumulates
+        // (the epilogue zeroes TMEM before releasing it), so the interleaving of the two
+        // warps' MMAs cannot change the exact integer level sums.  b_empty and tmem_full
+        // take one commit from each warp.
         constexpr int kMaxBlk = 256 / NC;  // window blocks per instruction (N <= 256)
-        // TMEM column of A-slice p's window: region t(p) = (p-1)/G (INT32 sub-group).
-        // In the first k-block of a period a window's blocks [0, x) were already written by
-        // an earlier window of the same region; blocks [x, L) are new (accumulate = 0).
+        const uint32_t me = warp - 5;
+        // TMEM column of A-slice p's window: region t(p) = (p-1)/G (INT32 sub-group)
         uint32_t pcol[S + 1];
-        int xinit[S + 1];
-        {
-            int seen[2] = {0, 0};
 #pragma unroll
-            for (int i = 0; i < S; ++i) {
-                const int p = i + 1;
-                const int t = (p - 1) / P.G;
-                pcol[p] = tmem_base + P.region_col[t];
-                const int L = S + 1 - p;
-                xinit[p] = seen[t];
-                seen[t] = seen[t] > L ? seen[t] : L;
-            }
-        }
+        for (int p = 1; p <= S; ++p) pcol[p] = tmem_base + P.region_col[(p - 1) / P.G];
         int bs = 0, as = 0;
-        uint32_t bph = 0, aph = 0;
+        uint32_t bph = 0, aph = 0, tpar = 0;
         uint32_t acc_iter = 0;
         long long st_b = 0, st_b0 = 0, st_a = 0, st_t = 0, st_af = 0, t_begin = clock64();
         const uint64_t adesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smA));
         const uint64_t bdesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smB));
 
-        // MMAs of A-slice p for one k-step against its window [0, L) (blocks [x, L) are
-        // initialised when init).
-        auto issue = [&](int p, uint64_t ad, uint64_t bd, bool init, int x) {
+        // MMAs of A-slice p for one k-step against its window [0, L)
+        auto issue = [&](int p, uint64_t ad, uint64_t bd) {
             const int L = S + 1 - p;
-            if (init) {
-                for (int j0 = 0; j0 < x; j0 += kMaxBlk) {
-                    const int nbk = (x - j0) < kMaxBlk ? (x - j0) : kMaxBlk;
-                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad,
-                                bd + (uint64_t)((j0 * NC * kKB) >> 4),
-                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 1u);
-                }
-                for (int j0 = x; j0 < L; j0 += kMaxBlk) {
-                    const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
-                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad,
-                                bd + (uint64_t)((j0 * NC * kKB) >> 4),
-                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 0u);
-                }
-            } else {
 #pragma unroll
-                for (int j0 = 0; j0 < L; j0 += kMaxBlk) {
-                    const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
-                    ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad,
-                                bd + (uint64_t)((j0 * NC * kKB) >> 4),
-                                ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 1u);
-                }
+            for (int j0 = 0; j0 < L; j0 += kMaxBlk) {
+                const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
+                ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad, bd + (uint64_t)((j0 * NC * kKB) >> 4),
+                            ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 1u);
             }
         };
 
@@ -356,6 +346,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t kb0 = (int64_t)c * P.chunk_blocks;
                 int64_t kb1 = kb0 + P.chunk_blocks;
                 kb1 = kb1 < P.num_k_blocks ? kb1 : P.num_k_blocks;
+                // the epilogue has read and zeroed the accumulator (phase acc_iter)
+                {
+                    long long c0 = P.stats ? clock64() : 0;
+                    ptx::mbar_wait(tmem_empty, acc_iter & 1);
+                    if (P.stats) st_t += clock64() - c0;
+                    ptx::tc_fence_after();
+                }
                 for (int64_t kb = kb0; kb < kb1; ++kb) {
                     long long c1 = P.stats ? clock64() : 0;
                     ptx::mbar_wait(&b_full[bs], bph);
@@ -364,58 +361,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else st_b += clock64() - c1;
                     }
                     const uint64_t bdesc0 = bdesc_base + ((bs * P.b_stage_bytes) >> 4);
-                    if (kb == kb0) {
-                        // ---- first k-block of the period: wait for the epilogue to release
-                        // the accumulator, initialise TMEM blocks on first write ----
-                        long long c0 = P.stats ? clock64() : 0;
-                        ptx::mbar_wait(tmem_empty, (acc_iter & 1) ^ 1);
-                        if (P.stats) st_t += clock64() - c0;
-                        ptx::tc_fence_after();
 #pragma unroll
-                        for (int i = 0; i < S; ++i) {
-                            const int p = i + 1;
-                            const int L = S + 1 - p;
+                    for (int i = 0; i < S; ++i) {
+                        const int p = slice_p(S, i);
+                        // tile parity: tpar flips every tile (S is folded in by the counter)
+                        if (((tpar + (uint32_t)i) & 1u) == me) {
                             long long c2 = P.stats ? clock64() : 0;
                             ptx::mbar_wait(&a_full[as], aph);
-                            if (P.stats) st_af += clock64() - c2;
-                            ptx::tc_fence_after();
-                            if (ptx::elect_one()) {
-                                const uint64_t adesc0 = adesc_base + ((as * P.a_stage_bytes) >> 4);
-                                const int x = xinit[p] < L ? xinit[p] : L;
-#pragma unroll
-                                for (int ks = 0; ks < kKB / 32; ++ks)
-                                    issue(p, adesc0 + (uint64_t)(ks * 2),
-                                          bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4),
-                                          ks == 0, x);
-                                if (P.cl == 2) ptx::mma_commit_mc(&a_empty[as], (uint16_t)0x3);
-                                else ptx::mma_commit(&a_empty[as]);
+                            if (P.stats) {
+                                if (kb == kb0) st_af += clock64() - c2;
+                                else st_a += clock64() - c2;
                             }
-                            __syncwarp();
-                            if (++as == P.a_stages) { as = 0; aph ^= 1; }
-                        }
-                    } else {
-                        // ---- steady state: ascending p, fully unrolled ----
-#pragma unroll
-                        for (int i = 0; i < S; ++i) {
-                            const int p = i + 1;
-                            long long c2 = P.stats ? clock64() : 0;
-                            ptx::mbar_wait(&a_full[as], aph);
-                            if (P.stats) st_a += clock64() - c2;
                             ptx::tc_fence_after();
                             if (ptx::elect_one()) {
                                 const uint64_t adesc0 = adesc_base + ((as * P.a_stage_bytes) >> 4);
 #pragma unroll
                                 for (int ks = 0; ks < kKB / 32; ++ks)
                                     issue(p, adesc0 + (uint64_t)(ks * 2),
-                                          bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4),
-                                          false, 0);
+                                          bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4));
                                 if (P.cl == 2) ptx::mma_commit_mc(&a_empty[as], (uint16_t)0x3);
                                 else ptx::mma_commit(&a_empty[as]);
                             }
                             __syncwarp();
-                            if (++as == P.a_stages) { as = 0; aph ^= 1; }
                         }
+                        if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
+                    tpar += (uint32_t)S;
                     if (ptx::elect_one()) ptx::mma_commit(&b_empty[bs]);
                     __syncwarp();
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
@@ -424,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
             }
         }
-        if (P.stats && lane == 0) {
+        if (P.stats && lane == 0 && me == 0) {
             long long *st = P.stats + (int64_t)blockIdx.x * kStatSlots;
             st[ST_TOTAL] = clock64() - t_begin;
             st[ST_MMA_WAIT_B] = st_b;
@@ -446,6 +417,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int T = P.T;
         const int G = P.G;
         constexpr int kCH = NC < 32 ? NC : 32;  // columns per TMEM read batch
+        // The MMA issuers only accumulate: this warp zeroes its 32 TMEM lanes of every column
+        // it reads (after reading them) and, once, before the first period.
+        {
+            const uint32_t used = (uint32_t)(S * NC) + (T > 1 ? (uint32_t)((S - G) * NC) : 0u);
+            for (uint32_t c = 0; c < used; c += 16) ptx::tmem_st_zero_x16(tmem_base + lane_addr + c);
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(tmem_empty);  // phase 0: accumulator zeroed
+        }
         uint32_t acc_iter = 0, tile_iter = 0;
         long long st_e = 0, st_et = 0, st_es = 0;
         for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl) {
@@ -493,6 +473,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                         ptx::tmem_ld_x16(tmem_base + lane_addr + P.region_col[1] +
                                                              (uint32_t)(j * NC + c0 + c16), &v2[c16]);
                                 ptx::tmem_ld_wait();
+#pragma unroll
+                                for (int c16 = 0; c16 < kCH; c16 += 16)
+                                    if (c0 + c16 < NC) {
+                                        ptx::tmem_st_zero_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16));
+                                        ptx::tmem_st_zero_x16(tmem_base + lane_addr + P.region_col[1] +
+                                                              (uint32_t)(j * NC + c0 + c16));
+                                    }
                                 // acc += L_g 2^(-wg): the product is exact, so the fma rounds
                                 // once like the oracle's add; both INT32 parts and their sum
                                 // are exact in binary64.
@@ -505,14 +492,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                             } else {
                                 ptx::tmem_ld_wait();
 #pragma unroll
+                                for (int c16 = 0; c16 < kCH; c16 += 16)
+                                    if (c0 + c16 < NC)
+                                        ptx::tmem_st_zero_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16));
+#pragma unroll
                                 for (int ii = 0; ii < kCH; ++ii)
                                     if (c0 + ii < NC)
                                         acc[c0 + ii] = __fma_rn((double)(int32_t)v[ii], sc, acc[c0 + ii]);
                             }
                         }
                     }
+                    ptx::tmem_st_wait();
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(tmem_empty);  // accumulator free: next period may start
+                    ptx::mbar_arrive(tmem_empty);  // accumulator read and zeroed: next period may start
                     if (P.stats) st_et += clock64() - ce;
                     long long cs0 = P.stats ? clock64() : 0;
                     if (row_ok) store_row<NC>(P, acc, ebt, ea, row, nb);
@@ -545,6 +537,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         ptx::tmem_ld_wait();
 #pragma unroll
+                        for (int c16 = 0; c16 < kCH; c16 += 16) {
+                            if (c0 + c16 >= NC) break;
+                            ptx::tmem_st_zero_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16));
+                            if (two)
+                                ptx::tmem_st_zero_x16(tmem_base + lane_addr + P.region_col[1] +
+                                                      (uint32_t)(j * NC + c0 + c16));
+                        }
+#pragma unroll
                         for (int ii = 0; ii < kCH; ++ii) {
                             const int i = c0 + ii;
                             if (i >= NC) break;
@@ -573,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
+                ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(tmem_empty);
                 if (last && fp_out && row_ok) store_row<NC>(P, acc, ebt, ea, row, nb);

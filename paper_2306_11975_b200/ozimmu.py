@@ -13,7 +13,8 @@ import ctypes as ct
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libozimmu.so")
+# OZIMMU_LIB: development override (a variants/ build of the same sources)
+LIB_PATH = os.environ.get("OZIMMU_LIB") or os.path.join(HERE, "libozimmu.so")
 
 OP = {"N": 0, "T": 1, "C": 2, 0: 0, 1: 1, 2: 2}
 STATUS = {0: "OZIMMU_SUCCESS", 1: "OZIMMU_ERR_INVALID_VALUE", 2: "OZIMMU_ERR_UNSUPPORTED",

@@ -17,8 +17,14 @@ __global__ void __launch_bounds__(128, 1) k_bench(const int *ns, int nn, int rou
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     const int warp = threadIdx.x / 32;
-    for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
-        reinterpret_cast<int4 *>(smem)[i] = make_int4(0, 0, 0, 0);
+    // mode 0/1: zeros; mode >= 2: pseudo-random bytes (the Ozaki digit planes are ~uniform
+    // in [-127, 127], which toggles the MAC array and changes power, not cycles)
+    for (int i = threadIdx.x; i < 168 * 1024 / 16; i += blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x * 97u;
+        h ^= h >> 13; h *= 0x5bd1e995u; h ^= h >> 15;
+        reinterpret_cast<int4 *>(smem)[i] = mode >= 2 ? make_int4(h, h * 3u + 1u, h * 7u + 5u, h ^ 0xdeadbeefu)
+                                                   : make_int4(0, 0, 0, 0);
+    }
     if (threadIdx.x == 0) { ptx::mbar_init(&bar, 1); ptx::fence_mbar_init(); }
     if (warp == 0) { ptx::tmem_alloc(&tslot, 512); ptx::tmem_relinquish(); }
     asm volatile("fence.proxy.async.shared::cta;");
@@ -28,14 +34,19 @@ __global__ void __launch_bounds__(128, 1) k_bench(const int *ns, int nn, int rou
     const uint32_t tmem = tslot;
     if (warp == 1) {
         if (ptx::elect_one()) {
-            const uint32_t a = ptx::smem_u32(smem), b = a + 16384;
+            // mode 3: A rotates over a 7-tile ring (16 KB each) and B sits after it, with the
+            // s = 9 window offsets (as in k_oz_gemm); modes 0-2: fixed addresses
+            const uint32_t a0 = ptx::smem_u32(smem);
+            const uint32_t b = mode == 3 ? a0 + 7 * 16384 : a0 + 16384;
             long long t0 = clock64();
             for (int r = 0; r < rounds; ++r) {
                 for (int i = 0; i < nn; ++i) {
                     const int N = ns[i];
                     for (int ks = 0; ks < 4; ++ks) {
+                        const uint32_t a = mode == 3 ? a0 + (uint32_t)(((r * nn + i) % 7) * 16384) : a0;
+                        const uint32_t boff = mode == 3 ? (uint32_t)((i % 9) * 48 * 128) : 0u;
                         uint64_t ad = ptx::smem_desc_kmajor<128>(a + ks * 32);
-                        uint64_t bd = ptx::smem_desc_kmajor<128>(b + ks * 32);
+                        uint64_t bd = ptx::smem_desc_kmajor<128>(b + boff + ks * 32);
                         uint32_t col = mode == 0 ? 0u : (uint32_t)((i % 2) * 256);
                         ptx::mma_i8(tmem + col, ad, bd, ptx::idesc_i8(128, N), 1u);
                     }
@@ -67,21 +78,21 @@ int main() {
     long long *d_cyc;
     cudaMalloc(&d_ns, 64 * sizeof(int));
     cudaMalloc(&d_cyc, sizeof(long long));
-    cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 170 * 1024);
+    cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int mode = 0; mode < 2; ++mode)
+    for (int mode = 0; mode < 4; ++mode)
         for (auto &mx : mixes) {
             cudaMemcpy(d_ns, mx.second.data(), mx.second.size() * sizeof(int), cudaMemcpyHostToDevice);
             long long ntot = 0;
             for (int n : mx.second) ntot += n;
             const int rounds = 2000;
-            k_bench<<<sms, 128, 170 * 1024>>>(d_ns, (int)mx.second.size(), rounds, d_cyc, mode);
+            k_bench<<<sms, 128, 200 * 1024>>>(d_ns, (int)mx.second.size(), rounds, d_cyc, mode);
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
             cudaEventCreate(&e1);
             cudaEventRecord(e0);
-            k_bench<<<sms, 128, 170 * 1024>>>(d_ns, (int)mx.second.size(), rounds, d_cyc, mode);
+            k_bench<<<sms, 128, 200 * 1024>>>(d_ns, (int)mx.second.size(), rounds, d_cyc, mode);
             cudaEventRecord(e1);
             cudaError_t err = cudaDeviceSynchronize();
             float ms = 0;
