@@ -58,6 +58,9 @@ __host__ __device__ constexpr int nc_for(int S) {
 // s-1, ... (long and short windows alternate, so the two MMA issuers get similar work; the
 // ascending order measured the same).  The level sums are exact integers, so the order of
 // the MMAs into TMEM does not change any result.
+#ifndef OZ_KSNAKE
+#define OZ_KSNAKE 1
+#endif
 #ifndef OZ_SLICE_ORDER
 #define OZ_SLICE_ORDER 1
 #endif
@@ -258,17 +261,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 long long c0 = P.stats ? clock64() : 0;
                 wave_sync(P, wave);
                 if (P.stats) st_w += clock64() - c0;
+                // K snake: odd waves walk K backwards, so a wave starts on the k-blocks the
+                // previous wave (same A row blocks) touched last, still in L2.  The INT32
+                // sums are order-independent; K chunks (int64 partials) keep the forward order.
+                const bool rev = OZ_KSNAKE && P.k_chunks == 1 && (wave & 1);
+                auto kmap = [&](int64_t kb) { return rev ? P.num_k_blocks - 1 - kb : kb; };
                 for (int64_t kb = 0; kb < P.prefetch_kb && kb < P.num_k_blocks; ++kb)
-                    prefetch(kb, mb, nb);
+                    prefetch(kmap(kb), mb, nb);
                 for (int64_t kb = 0; kb < P.num_k_blocks; ++kb) {
                     if (P.prefetch_kb && kb + P.prefetch_kb < P.num_k_blocks)
-                        prefetch(kb + P.prefetch_kb, mb, nb);
+                        prefetch(kmap(kb + P.prefetch_kb), mb, nb);
+                    const int64_t kx = kmap(kb);
                     long long c1 = P.stats ? clock64() : 0;
                     ptx::mbar_wait(&b_empty[bs], bph ^ 1);
                     if (P.stats) st_pb += clock64() - c1;
                     ptx::mbar_arrive_expect_tx(&b_full[bs], b_tx);
                     ptx::tma_load_3d(&tmB, &b_full[bs], smB + (size_t)bs * P.b_stage_bytes,
-                                     (int32_t)(kb * kKB), (int32_t)(nb * NC), 0,
+                                     (int32_t)(kx * kKB), (int32_t)(nb * NC), 0,
                                      ptx::kEvictNormal);
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
 #pragma unroll 1
@@ -281,13 +290,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ptx::tma_load_3d_mc(&tmA, &a_full[as],
                                                 smA + (size_t)as * P.a_stage_bytes +
                                                     rank * (kBlockM / 2) * kKB,
-                                                (int32_t)(kb * kKB),
+                                                (int32_t)(kx * kKB),
                                                 (int32_t)(mb * kBlockM + rank * (kBlockM / 2)),
                                                 slice_p(S, i) - 1,
                                                 (uint16_t)0x3, ptx::kEvictNormal);
                         else
                             ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
-                                             (int32_t)(kb * kKB), (int32_t)(mb * kBlockM),
+                                             (int32_t)(kx * kKB), (int32_t)(mb * kBlockM),
                                              slice_p(S, i) - 1, ptx::kEvictNormal);
                         if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
@@ -642,13 +651,20 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
     if (e != cudaSuccess) return e;
-    // Optional CTA pairs (clusters of 2) sharing the A tiles by TMA multicast (half the A
-    // bytes per SM from L2), OZIMMU_CLUSTER=2.  Off by default: measured 8% slower at
-    // 16384^3, s = 9 (the pair runs in lockstep; the A-ring waits are not L2-bandwidth
-    // bound -- DESIGN.md section 5).  The grid is sized to the co-resident clusters.
-    static const int cl_env = getenv("OZIMMU_CLUSTER") ? atoi(getenv("OZIMMU_CLUSTER")) : 1;
+    // CTA pairs (clusters of 2) sharing the A tiles by TMA multicast: each CTA loads half of
+    // every A-slice tile and multicasts it to both, halving the A bytes per SM from L2 (the
+    // larger operand stream: 128 rows x s slices per k-block vs NC x s for B).  Measured at
+    // 16384^3, s = 9: +1.7% (less L2 traffic -> more clock under the power cap).  Pairs take
+    // column tiles (2j, 2j+1); an odd column-tile count leaves one dummy tile per row block,
+    // so pairs are used only when that waste is small.  OZIMMU_CLUSTER=1 forces single CTAs.
+#ifndef OZ_CLUSTER_DEFAULT
+#define OZ_CLUSTER_DEFAULT 2
+#endif
+    static const int cl_env =
+        getenv("OZIMMU_CLUSTER") ? atoi(getenv("OZIMMU_CLUSTER")) : OZ_CLUSTER_DEFAULT;
     const int64_t tiles_m = ceil_div(a.m, kBlockM), tiles_n = ceil_div(a.n, NC);
-    int cl = (cl_env == 2 && tiles_n >= 2 && p.grid >= 2) ? 2 : 1;
+    int cl = (cl_env == 2 && tiles_n >= 2 && (tiles_n % 2 == 0 || tiles_n >= 32) && p.grid >= 2)
+                 ? 2 : 1;
     int grid = p.grid;
     cudaLaunchAttribute attr[1];
     if (cl == 2) {

@@ -1,7 +1,8 @@
-"""The optional CTA-pair variant of the fused GEMM (OZIMMU_CLUSTER=2: clusters of two CTAs,
-A tiles TMA-multicast to both, dummy tile when the column-tile count is odd) must give the
-same bits as the default kernel: re-run the DGEMM / ZGEMM / batched parity suites with it
-enabled (the variable is read once per process, hence the subprocess)."""
+"""The fused GEMM runs by default as CTA pairs (clusters of two CTAs, A tiles TMA-multicast
+to both, dummy tile when the column-tile count is odd); OZIMMU_CLUSTER=1 forces single CTAs.
+Both must give the same bits: the default suites cover the pairs, this re-runs the DGEMM /
+ZGEMM / batched parity suites with single CTAs (the variable is read once per process,
+hence the subprocess)."""
 import os
 import subprocess
 import sys
@@ -13,8 +14,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_parity_suites_with_cta_pairs():
-    env = dict(os.environ, OZIMMU_CLUSTER="2")
+def test_parity_suites_with_single_ctas():
+    env = dict(os.environ, OZIMMU_CLUSTER="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"),
                         os.path.join(ROOT, "tests", "test_gpu_zgemm.py"),

@@ -67,7 +67,8 @@ def child(N, s, iters, trans):
     clk = sorted(x[0] for x in samples)
     pw = sorted(x[1] for x in samples)
     hsh = hashlib.sha1(C.cpu().numpy().tobytes()).hexdigest()[:12]
-    print(json.dumps({"lib": os.path.basename(os.environ.get("OZIMMU_LIB", "default")), "N": N,
+    print(json.dumps({"lib": os.path.basename(os.environ.get("OZIMMU_LIB", "default")),
+                      "env": os.environ.get("AB_TAG", ""), "N": N,
                       "s": s, "ms": round(ms, 3), "tflops": round(2.0 * N ** 3 / ms / 1e9, 2),
                       "min_ms": round(ts[0], 3), "max_ms": round(ts[-1], 3),
                       "sm_mhz": clk[len(clk) // 2] if clk else None,
@@ -89,8 +90,14 @@ def main():
     for _ in range(int(opts["--rounds"])):
         for lib in libs:
             env = dict(os.environ)
+            # "lib@VAR=val,VAR2=val" runs the variant with extra environment
+            lib, _, extra = lib.partition("@")
+            for kv in filter(None, extra.split(",")):
+                k, _, v = kv.partition("=")
+                env[k] = v
             if lib != "default":
                 env["OZIMMU_LIB"] = os.path.abspath(lib)
+            env["AB_TAG"] = extra
             subprocess.run([sys.executable, __file__, "--child", str(N), str(s), opts["--iters"],
                             opts["--trans"]], env=env, check=False)
 

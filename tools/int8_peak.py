@@ -13,6 +13,7 @@ import json
 import os
 import subprocess
 import sys
+import threading
 import time
 
 import torch
@@ -40,18 +41,24 @@ def run(fn, ops, secs=4.0):
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1))
-    # sustained
+    # sustained: back to back for `secs`, clocks sampled by a side thread (never stalls the GPU)
     samples = []
-    n = 0
-    t_end = time.time() + secs
+    stop = threading.Event()
+
+    def sampler():
+        while not stop.is_set():
+            samples.append(smi())
+            time.sleep(0.2)
+    th = threading.Thread(target=sampler, daemon=True)
+    n = max(4, int(secs * 1e3 / best))
+    th.start()
     e0.record()
-    while time.time() < t_end:
-        for _ in range(4):
-            fn()
-            n += 1
-        samples.append(smi())
+    for _ in range(n):
+        fn()
     e1.record()
     torch.cuda.synchronize()
+    stop.set()
+    th.join()
     ms = e0.elapsed_time(e1) / n
     clk = sorted(s[0] for s in samples if s[0])
     pw = sorted(s[1] for s in samples if s[1])
