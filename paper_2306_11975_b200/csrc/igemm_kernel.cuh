@@ -339,14 +339,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t adesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smA));
         const uint64_t bdesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smB));
 
-        // MMAs of A-slice p for one k-step against its window [0, L)
+        // MMAs of A-slice p for one k-step against its window [0, L), split into the fewest
+        // instructions of N <= 256 with block counts as equal as possible: an M = 128,
+        // K = 32 i8 MMA costs about max(N/2, ~58) cycles (tools/mma_bench.cu), so 6 blocks
+        // go as 3 + 3 rather than 5 + 1.
         auto issue = [&](int p, uint64_t ad, uint64_t bd) {
             const int L = S + 1 - p;
+            const int pieces = (L + kMaxBlk - 1) / kMaxBlk;
+            int j0 = 0;
 #pragma unroll
-            for (int j0 = 0; j0 < L; j0 += kMaxBlk) {
-                const int nbk = (L - j0) < kMaxBlk ? (L - j0) : kMaxBlk;
+            for (int q = 0; q < pieces; ++q) {
+                const int nbk = L / pieces + (q < L % pieces ? 1 : 0);
                 ptx::mma_i8(pcol[p] + (uint32_t)(j0 * NC), ad, bd + (uint64_t)((j0 * NC * kKB) >> 4),
                             ptx::idesc_i8(kBlockM, (uint32_t)(nbk * NC)), 1u);
+                j0 += nbk;
             }
         };
 

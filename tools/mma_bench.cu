@@ -71,6 +71,9 @@ int main() {
         {"N64x8", {64, 64, 64, 64, 64, 64, 64, 64}},
         {"N48x8", {48, 48, 48, 48, 48, 48, 48, 48}},
         {"s9nc48", {240, 192, 240, 144, 240, 96, 240, 48, 240, 192, 144, 96, 48}},
+        {"s9bal", {240, 192, 192, 192, 192, 144, 144, 144, 240, 192, 144, 96, 48}},
+        {"N96x8", {96, 96, 96, 96, 96, 96, 96, 96}},
+        {"N144x8", {144, 144, 144, 144, 144, 144, 144, 144}},
         {"s9nc32", {256, 32, 256, 224, 192, 160, 128, 96, 64, 32}},
         {"s7nc64", {256, 192, 256, 128, 256, 64, 256, 192, 128, 64}},
     };
@@ -81,7 +84,7 @@ int main() {
     cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int mode = 0; mode < 4; ++mode)
+    for (int mode = 2; mode < 4; ++mode)
         for (auto &mx : mixes) {
             cudaMemcpy(d_ns, mx.second.data(), mx.second.size() * sizeof(int), cudaMemcpyHostToDevice);
             long long ntot = 0;
