@@ -261,8 +261,9 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
                        const int8_t *b_planes, const int32_t *EB, int64_t b_plane_rows,
                        double alpha, double beta, double *C, int64_t ldc, int64_t *scratch,
                        unsigned int *sync, int *launches, BatchMap crow = BatchMap(),
-                       BatchMap ccol = BatchMap()) {
+                       BatchMap ccol = BatchMap(), int64_t a_plane_rows = 0) {
     GemmArgs ga{};
+    ga.a_plane_rows = a_plane_rows;
     ga.c_rows = crow;
     ga.c_cols = ccol;
     ga.a_planes = a_planes;
@@ -967,10 +968,13 @@ ozimmu_status_t ozimmu_zgemm_strided_batched(ozimmu_handle_t h, ozimmu_op_t tran
 // with events; the call blocks until C is back in host memory.
 namespace {
 
+// Host-buffer pipeline (ozimmu_dgemm_host): op(A) in P row blocks of mb rows, op(B) in J
+// column chunks of nb columns.  Device buffers: the full A planes [s][m][k_pad] + E_A, the
+// full B-slice buffer, double-buffered FP64 staging for one A block / one B chunk, C (m x n,
+// ld m) and the GEMM scratch.
 struct HostPlan {
     int64_t mb, nb, P, J;
-    size_t bbuf, bst, ast, apl, cst, keys, sync, scratch, total;
-    size_t o_bbuf, o_bst[2], o_ast[2], o_apl[2], o_cst[2], o_keys, o_sync, o_scratch;
+    size_t o_apl, o_bbuf, o_ast[2], o_bst[2], o_c, o_keys, o_sync, o_scratch, total;
 };
 
 bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPlan *hp) {
@@ -979,7 +983,7 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     static const int64_t env_mb = getenv("OZIMMU_HOST_MB") ? atoll(getenv("OZIMMU_HOST_MB")) : 0;
     static const int64_t env_nb = getenv("OZIMMU_HOST_NB") ? atoll(getenv("OZIMMU_HOST_NB")) : 0;
     int64_t mb = env_mb > 0 ? env_mb : round_up(ceil_div(m, 8), 128);
-    int64_t nb = env_nb > 0 ? env_nb : round_up(ceil_div(n, 8), 64);
+    int64_t nb = env_nb > 0 ? env_nb : round_up(ceil_div(n, 8), 96);
     if (mb < 512) mb = 512;
     if (nb < 512) nb = 512;
     if (mb > m) mb = m;
@@ -989,30 +993,28 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     hp->P = ceil_div(m, mb);
     hp->J = ceil_div(n, nb);
     size_t scratch = 0;
-    const int64_t shapes[3][2] = {{mb, nb}, {mb, n}, {m - (hp->P - 1) * mb, n}};
+    const int64_t shapes[3][2] = {{mb, nb}, {m, nb}, {mb, n}};
     for (auto &sh : shapes) {
         GemmPlan gp;
         if (!plan_gemm(s, w, sh[0], sh[1], k_pad, h->num_sms, &gp)) return false;
         const size_t c = chunk_scratch_bytes(gp, s);
         if (c > scratch) scratch = c;
     }
-    hp->bbuf = b_buf_bytes(n, k_pad, s);
-    hp->bst = align_up((size_t)k * nb * sizeof(double));
-    hp->ast = align_up((size_t)mb * k * sizeof(double));
-    hp->apl = align_up((size_t)s * mb * k_pad) + align_up(sizeof(int32_t) * (size_t)mb);
-    hp->cst = align_up((size_t)mb * n * sizeof(double));
-    hp->keys = align_up(sizeof(int32_t) * (size_t)(mb > nb ? mb : nb));
-    hp->sync = kAlign;
-    hp->scratch = align_up(scratch);
     size_t off = 0;
-    hp->o_bbuf = off; off += hp->bbuf;
-    for (int i = 0; i < 2; ++i) { hp->o_bst[i] = off; off += hp->bst; }
-    for (int i = 0; i < 2; ++i) { hp->o_ast[i] = off; off += hp->ast; }
-    for (int i = 0; i < 2; ++i) { hp->o_apl[i] = off; off += hp->apl; }
-    for (int i = 0; i < 2; ++i) { hp->o_cst[i] = off; off += hp->cst; }
-    hp->o_keys = off; off += hp->keys;
-    hp->o_sync = off; off += hp->sync;
-    hp->o_scratch = off; off += hp->scratch;
+    hp->o_apl = off;
+    off += align_up((size_t)s * m * k_pad) + align_up(sizeof(int32_t) * (size_t)m);
+    hp->o_bbuf = off;
+    off += b_buf_bytes(n, k_pad, s);
+    for (int i = 0; i < 2; ++i) { hp->o_ast[i] = off; off += align_up((size_t)mb * k * sizeof(double)); }
+    for (int i = 0; i < 2; ++i) { hp->o_bst[i] = off; off += align_up((size_t)k * nb * sizeof(double)); }
+    hp->o_c = off;
+    off += align_up((size_t)m * n * sizeof(double));
+    hp->o_keys = off;
+    off += align_up(sizeof(int32_t) * (size_t)(mb > nb ? mb : nb));
+    hp->o_sync = off;
+    off += kAlign;
+    hp->o_scratch = off;
+    off += align_up(scratch);
     hp->total = off;
     return true;
 }
@@ -1107,9 +1109,12 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     st = host_buffers(h, hp.total);
     if (st) return st;
     uint8_t *base = static_cast<uint8_t *>(h->host_buf);
+    int8_t *a_planes = reinterpret_cast<int8_t *>(base + hp.o_apl);
+    int32_t *EA = reinterpret_cast<int32_t *>(base + hp.o_apl + align_up((size_t)s * m * k_pad));
     uint8_t *bbuf = base + hp.o_bbuf;
     int8_t *b_planes = reinterpret_cast<int8_t *>(bbuf);
     int32_t *EB = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
+    double *dC = reinterpret_cast<double *>(base + hp.o_c);
     int32_t *keys = reinterpret_cast<int32_t *>(base + hp.o_keys);
     int64_t *scratch = reinterpret_cast<int64_t *>(base + hp.o_scratch);
     unsigned int *sync = reinterpret_cast<unsigned int *>(base + hp.o_sync);
@@ -1117,9 +1122,13 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     const bool a_rows_contig = transA != OZIMMU_OP_N;  // device copy of a row block
     const bool b_cols_contig = transB == OZIMMU_OP_N;
 
-    // events: [0] start, then per block / chunk
+    // Transfers alternate between A row blocks and B column chunks (A_0, B_0, A_1, B_1, ...),
+    // so the computable part of C grows as a square: after A_i arrives, C block row i
+    // against the chunks already sliced is one GEMM; after B_j arrives, C chunk j against the
+    // row blocks already sliced is one GEMM.  The tensor cores start after the first block
+    // and chunk, and every C region goes back to the host as soon as its GEMM is done.
     const int64_t P = hp.P, J = hp.J;
-    const int64_t n_ev = 1 + 5 * P + 2 * J;
+    const int64_t n_ev = 1 + 2 * P + 2 * J + 3 * (P + J);
     cudaEvent_t *ev = static_cast<cudaEvent_t *>(calloc((size_t)n_ev, sizeof(cudaEvent_t)));
     if (!ev) return OZIMMU_ERR_WORKSPACE;
     cudaError_t e = cudaSuccess;
@@ -1127,9 +1136,10 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     for (; made < n_ev && e == cudaSuccess; ++made)
         e = cudaEventCreateWithFlags(&ev[made], cudaEventDisableTiming);
     cudaEvent_t ev_start = ev[0];
-    cudaEvent_t *ev_ain = ev + 1, *ev_afree = ev + 1 + P, *ev_cin = ev + 1 + 2 * P;
-    cudaEvent_t *ev_cdone = ev + 1 + 3 * P, *ev_cout = ev + 1 + 4 * P;
-    cudaEvent_t *ev_bin = ev + 1 + 5 * P, *ev_bfree = ev + 1 + 5 * P + J;
+    cudaEvent_t *ev_ain = ev + 1, *ev_afree = ev_ain + P, *ev_bin = ev_afree + P,
+                *ev_bfree = ev_bin + J, *ev_cin = ev_bfree + J, *ev_cdone = ev_cin + (P + J),
+                *ev_cout = ev_cdone + (P + J);
+    int64_t nreg = 0;  // C regions issued
     int launches = 0;
     cudaStream_t cs = h->stream;
 #define OZ_TRY(x) do { if (e == cudaSuccess) e = (x); } while (0)
@@ -1137,86 +1147,69 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_start, 0));
     OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_start, 0));
 
-    auto block_rows = [&](int64_t i) { return (i == P - 1) ? m - i * hp.mb : hp.mb; };
-    auto copy_a = [&](int64_t i) {
-        const int64_t r0 = i * hp.mb, mi = block_rows(i);
-        double *dst = reinterpret_cast<double *>(base + hp.o_ast[i & 1]);
-        if (i >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_afree[i - 2], 0));
-        if (a_rows_contig)  // stored k x m: columns r0 .. r0+mi
-            OZ_TRY(copy2d(dst, k, A + r0 * lda, lda, k, mi, cudaMemcpyHostToDevice, h->h2d));
-        else  // stored m x k: rows r0 .. r0+mi of every column
-            OZ_TRY(copy2d(dst, mi, A + r0, lda, mi, k, cudaMemcpyHostToDevice, h->h2d));
-        OZ_TRY(cudaEventRecord(ev_ain[i], h->h2d));
+    auto rows_of = [&](int64_t i) { return (i == P - 1) ? m - i * hp.mb : hp.mb; };
+    auto cols_of = [&](int64_t j) { return (j == J - 1) ? n - j * hp.nb : hp.nb; };
+    // C region rows [r0, r0+mr) x cols [c0, c0+nc): (beta C in), GEMM, C out
+    auto region = [&](int64_t r0, int64_t mr, int64_t c0, int64_t nc) {
+        if (mr <= 0 || nc <= 0) return;
+        const int64_t q = nreg++;
+        double *dCr = dC + r0 + c0 * m;
         if (has_beta) {
-            if (i >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_cout[i - 2], 0));
-            OZ_TRY(copy2d(reinterpret_cast<double *>(base + hp.o_cst[i & 1]), mi, C + r0, ldc, mi,
-                          n, cudaMemcpyHostToDevice, h->h2d));
-            OZ_TRY(cudaEventRecord(ev_cin[i], h->h2d));
+            OZ_TRY(copy2d(dCr, m, C + r0 + c0 * ldc, ldc, mr, nc, cudaMemcpyHostToDevice, h->h2d));
+            OZ_TRY(cudaEventRecord(ev_cin[q], h->h2d));
+            OZ_TRY(cudaStreamWaitEvent(cs, ev_cin[q], 0));
         }
-    };
-    auto slice_a_block = [&](int64_t i) {
-        const int64_t mi = block_rows(i);
-        const double *src = reinterpret_cast<const double *>(base + hp.o_ast[i & 1]);
-        int8_t *pl = reinterpret_cast<int8_t *>(base + hp.o_apl[i & 1]);
-        int32_t *EA = reinterpret_cast<int32_t *>(base + hp.o_apl[i & 1] +
-                                                  align_up((size_t)s * hp.mb * k_pad));
-        OZ_TRY(cudaStreamWaitEvent(cs, ev_ain[i], 0));
-        OZ_TRY(launch_split(src, a_rows_contig ? k : mi, a_rows_contig, mi, k, k_pad, s, w,
-                            /*reverse=*/false, pl, mi * k_pad, EA, keys, h->num_sms, cs,
-                            &launches));
-        OZ_TRY(cudaEventRecord(ev_afree[i], cs));
-        if (has_beta) OZ_TRY(cudaStreamWaitEvent(cs, ev_cin[i], 0));
-        else if (i >= 2) OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[i - 2], 0));
-    };
-    auto gemm = [&](int64_t i, int64_t c0, int64_t nc) {
-        const int64_t mi = block_rows(i);
-        const int8_t *pl = reinterpret_cast<const int8_t *>(base + hp.o_apl[i & 1]);
-        const int32_t *EA = reinterpret_cast<const int32_t *>(base + hp.o_apl[i & 1] +
-                                                              align_up((size_t)s * hp.mb * k_pad));
-        double *dC = reinterpret_cast<double *>(base + hp.o_cst[i & 1]);
         GemmPlan gp;
-        if (!plan_gemm(s, w, mi, nc, k_pad, h->num_sms, &gp)) {
+        if (!plan_gemm(s, w, mr, nc, k_pad, h->num_sms, &gp)) {
             if (e == cudaSuccess) e = cudaErrorInvalidValue;
             return;
         }
-        OZ_TRY(fused_gemm(h, gp, mi, nc, k_pad, s, w, pl, EA, b_planes + c0 * k_pad, EB + c0, n,
-                          *alpha, *beta, dC + c0 * mi, mi, scratch, sync, &launches));
+        OZ_TRY(fused_gemm(h, gp, mr, nc, k_pad, s, w, a_planes + r0 * k_pad, EA + r0,
+                          b_planes + c0 * k_pad, EB + c0, n, *alpha, *beta, dCr, m, scratch,
+                          sync, &launches, BatchMap(), BatchMap(), m));
+        OZ_TRY(cudaEventRecord(ev_cdone[q], cs));
+        OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_cdone[q], 0));
+        OZ_TRY(copy2d(C + r0 + c0 * ldc, ldc, dCr, m, mr, nc, cudaMemcpyDeviceToHost, h->d2h));
+        OZ_TRY(cudaEventRecord(ev_cout[q], h->d2h));
     };
-    auto copy_c_out = [&](int64_t i) {
-        const int64_t mi = block_rows(i);
-        OZ_TRY(cudaEventRecord(ev_cdone[i], cs));
-        OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_cdone[i], 0));
-        OZ_TRY(copy2d(C + i * hp.mb, ldc, reinterpret_cast<const double *>(base + hp.o_cst[i & 1]),
-                      mi, mi, n, cudaMemcpyDeviceToHost, h->d2h));
-        OZ_TRY(cudaEventRecord(ev_cout[i], h->d2h));
-    };
-
-    copy_a(0);
-    slice_a_block(0);
-    for (int64_t j = 0; j < J; ++j) {
-        const int64_t c0 = j * hp.nb, nc = (j == J - 1) ? n - c0 : hp.nb;
-        double *dst = reinterpret_cast<double *>(base + hp.o_bst[j & 1]);
-        if (j >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_bfree[j - 2], 0));
-        if (b_cols_contig)  // stored k x n: columns c0 .. c0+nc
-            OZ_TRY(copy2d(dst, k, B + c0 * ldb, ldb, k, nc, cudaMemcpyHostToDevice, h->h2d));
-        else  // stored n x k: rows c0 .. c0+nc
-            OZ_TRY(copy2d(dst, nc, B + c0, ldb, nc, k, cudaMemcpyHostToDevice, h->h2d));
-        OZ_TRY(cudaEventRecord(ev_bin[j], h->h2d));
-        OZ_TRY(cudaStreamWaitEvent(cs, ev_bin[j], 0));
-        OZ_TRY(launch_split(dst, b_cols_contig ? k : nc, b_cols_contig, nc, k, k_pad, s, w,
-                            /*reverse=*/true, b_planes + c0 * k_pad, n * k_pad, EB + c0, keys,
-                            h->num_sms, cs, &launches));
-        OZ_TRY(cudaEventRecord(ev_bfree[j], cs));
-        gemm(0, c0, nc);
+    int64_t ia = 0, jb = 0;  // A blocks / B chunks sliced so far
+    while (ia < P || jb < J) {
+        const bool take_a = ia < P && (jb >= J || ia * J <= jb * P);
+        if (take_a) {
+            const int64_t i = ia, r0 = i * hp.mb, mi = rows_of(i);
+            double *dst = reinterpret_cast<double *>(base + hp.o_ast[i & 1]);
+            if (i >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_afree[i - 2], 0));
+            if (a_rows_contig)  // stored k x m: columns r0 .. r0+mi
+                OZ_TRY(copy2d(dst, k, A + r0 * lda, lda, k, mi, cudaMemcpyHostToDevice, h->h2d));
+            else  // stored m x k: rows r0 .. r0+mi of every column
+                OZ_TRY(copy2d(dst, mi, A + r0, lda, mi, k, cudaMemcpyHostToDevice, h->h2d));
+            OZ_TRY(cudaEventRecord(ev_ain[i], h->h2d));
+            OZ_TRY(cudaStreamWaitEvent(cs, ev_ain[i], 0));
+            OZ_TRY(launch_split(dst, a_rows_contig ? k : mi, a_rows_contig, mi, k, k_pad, s, w,
+                                /*reverse=*/false, a_planes + r0 * k_pad, m * k_pad, EA + r0,
+                                keys, h->num_sms, cs, &launches));
+            OZ_TRY(cudaEventRecord(ev_afree[i], cs));
+            ++ia;
+            region(r0, mi, 0, jb == J ? n : jb * hp.nb);
+        } else {
+            const int64_t j = jb, c0 = j * hp.nb, nc = cols_of(j);
+            double *dst = reinterpret_cast<double *>(base + hp.o_bst[j & 1]);
+            if (j >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_bfree[j - 2], 0));
+            if (b_cols_contig)  // stored k x n: columns c0 .. c0+nc
+                OZ_TRY(copy2d(dst, k, B + c0 * ldb, ldb, k, nc, cudaMemcpyHostToDevice, h->h2d));
+            else  // stored n x k: rows c0 .. c0+nc
+                OZ_TRY(copy2d(dst, nc, B + c0, ldb, nc, k, cudaMemcpyHostToDevice, h->h2d));
+            OZ_TRY(cudaEventRecord(ev_bin[j], h->h2d));
+            OZ_TRY(cudaStreamWaitEvent(cs, ev_bin[j], 0));
+            OZ_TRY(launch_split(dst, b_cols_contig ? k : nc, b_cols_contig, nc, k, k_pad, s, w,
+                                /*reverse=*/true, b_planes + c0 * k_pad, n * k_pad, EB + c0, keys,
+                                h->num_sms, cs, &launches));
+            OZ_TRY(cudaEventRecord(ev_bfree[j], cs));
+            ++jb;
+            region(0, ia == P ? m : ia * hp.mb, c0, nc);
+        }
     }
-    copy_c_out(0);
-    for (int64_t i = 1; i < P; ++i) {
-        copy_a(i);
-        slice_a_block(i);
-        gemm(i, 0, n);
-        copy_c_out(i);
-    }
-    OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[P - 1], 0));
+    for (int64_t q = 0; q < nreg; ++q) OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[q], 0));
     OZ_TRY(cudaStreamSynchronize(cs));
 #undef OZ_TRY
     if (e != cudaSuccess) {

@@ -704,12 +704,14 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
         }
     }
     CUtensorMap tmA, tmB;
-    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, cl == 2 ? kBlockM / 2 : kBlockM, 1))
+    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, cl == 2 ? kBlockM / 2 : kBlockM, 1,
+                  a.a_plane_rows))
         return cudaErrorInvalidValue;
     if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s, a.b_plane_rows))
         return cudaErrorInvalidValue;
     CUtensorMap tmApf;  // up to 8 A-slice tiles of a k-block per box (L2 prefetch only)
-    if (!make_map(&tmApf, a.a_planes, a.k_pad, a.m, a.s, kBlockM, (uint32_t)(a.s < 8 ? a.s : 8)))
+    if (!make_map(&tmApf, a.a_planes, a.k_pad, a.m, a.s, kBlockM, (uint32_t)(a.s < 8 ? a.s : 8),
+                  a.a_plane_rows))
         return cudaErrorInvalidValue;
     KParams P;
     P.m = a.m;

@@ -66,6 +66,7 @@ struct GemmArgs {
     const int8_t *a_planes;  // [s][m][k_pad], natural slice order
     const int8_t *b_planes;  // [s][n][k_pad], REVERSED slice order (index s - q)
     int64_t b_plane_rows;    // rows per B plane in memory (0 = n): column chunk of a larger buffer
+    int64_t a_plane_rows;    // rows per A plane in memory (0 = m): row block of a larger buffer
     BatchMap c_rows, c_cols; // stacked batches: row r / column j of C -> item and its offset
                              // (stride in elements of C: doubles, or complex for EPI_ZGEMM)
     const int32_t *EA, *EB;  // exponents (EPI_DGEMM only)
