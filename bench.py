@@ -521,9 +521,11 @@ def main():
                "bitexact_vs_device_call": same,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": ems, "wall_ms_per_step": wall, "steps": esteps,
-               "note": ("ozimmu_dgemm_host on pinned-host A, B -> C (row-block / column-chunk "
-                        "pipeline: H2D, slicing, GEMM and D2H overlapped on 3 streams; blocks "
-                        "until C is in host memory)") if world == 1 else
+               "note": ("ozimmu_dgemm_host on pinned-host A, B -> C (A row blocks and B column "
+                        "chunks transferred alternately, each followed by one GEMM over the newly "
+                        "computable C region, whose D2H starts as soon as it is done; H2D, "
+                        "slicing, GEMM and D2H overlap on 3 streams; blocks until C is in host "
+                        "memory)") if world == 1 else
                        "ozimmu_dgemm on pinned-host A,B -> C via cudaMemcpyAsync on the same "
                        "stream (rank-local bytes; root also copies B)"}
 
