@@ -334,10 +334,19 @@ def main():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # test hook (never set by the driver): OZIMMU_BENCH_ONE_DEVICE=1 maps every rank to cuda:0
+    # and uses gloo, so the N > 1 code path can be exercised on a one-GPU box (timings
+    # meaningless: the ranks share one GPU and gloo stages through the host)
+    one_dev = os.environ.get("OZIMMU_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

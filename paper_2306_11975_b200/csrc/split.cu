@@ -15,6 +15,7 @@
 // HBM-bound: read 8 B/element (the strided variant reads twice: exponent pass +
 // transposing slice pass), write s B/element.  128-bit loads, 64-bit stores.
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -180,52 +181,58 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
     __shared__ int32_t red[256 / 32];
     const int sub = threadIdx.x / TPR;
     const int t = threadIdx.x % TPR;
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * VPB + sub;
-    const bool active = r < rows;
-    const double *v = M + vec_off(active ? r : 0, ld, per_item, item_stride);
-    const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
     const int64_t nchunk = k_pad / 8;
+    // Persistent blocks (grid sized by the host to a few blocks per SM): the vectors in
+    // flight (grid x VPB x 8 k bytes) stay well inside L2, so pass 2 re-reads a vector from
+    // L2 instead of HBM.
+    for (int64_t rb = blockIdx.x; rb * VPB < rows; rb += gridDim.x) {
+        const int64_t r = rb * VPB + sub;
+        const bool active = r < rows;
+        const double *v = M + vec_off(active ? r : 0, ld, per_item, item_stride);
+        const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
 
-    // ---- pass 1: E = max exponent key ----
-    int32_t key = kKeyEmpty;
-    if (active) {
+        // ---- pass 1: E = max exponent key ----
+        int32_t key = kKeyEmpty;
+        if (active) {
+            for (int64_t c = t; c < nchunk; c += TPR) {
+                double x[8];
+                load8(v, c * 8, kdim, al16, x);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
+        if (TPR > 32) {
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+            __syncthreads();
+            key = red[0];
+#pragma unroll
+            for (int i = 1; i < TPR / 32; ++i) key = max(key, red[i]);
+            __syncthreads();  // red[] is rewritten by the next vector
+        }
+        if (!active) continue;
+        const int32_t Ev = key_to_exp(key);
+        if (t == 0) {
+            if (CPX == 2) {
+                E[2 * r] = Ev;
+                E[2 * r + 1] = Ev;
+            } else {
+                E[r] = Ev;
+            }
+        }
+        const bool bad = Ev == kExpNonFinite;
+
+        // ---- pass 2: digits ----
         for (int64_t c = t; c < nchunk; c += TPR) {
+            const int64_t l0 = c * 8;
             double x[8];
-            load8(v, c * 8, kdim, al16, x);
+            if (!bad) load8(v, l0, kdim, al16, x);
+            Digits<W, S> dg[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
+            for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
+            emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
         }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
-    if (TPR > 32) {
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
-        __syncthreads();
-        key = red[0];
-#pragma unroll
-        for (int i = 1; i < TPR / 32; ++i) key = max(key, red[i]);
-    }
-    if (!active) return;
-    const int32_t Ev = key_to_exp(key);
-    if (t == 0) {
-        if (CPX == 2) {
-            E[2 * r] = Ev;
-            E[2 * r + 1] = Ev;
-        } else {
-            E[r] = Ev;
-        }
-    }
-    const bool bad = Ev == kExpNonFinite;
-
-    // ---- pass 2: digits ----
-    for (int64_t c = t; c < nchunk; c += TPR) {
-        const int64_t l0 = c * 8;
-        double x[8];
-        if (!bad) load8(v, l0, kdim, al16, x);
-        Digits<W, S> dg[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-        emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
     }
 }
 
@@ -399,12 +406,19 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
                            int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
     // kdim / k_pad count doubles of the (embedded) vector: 2 per complex element
     if (contiguous) {
+        // persistent grid of `bps` blocks per SM (OZIMMU_SPLIT_BPS, default 4): <= 148 x 4
+        // vectors of 8 k bytes in flight (77 MB at k = 16384, inside the 126 MB L2)
+        static const int bps = getenv("OZIMMU_SPLIT_BPS") ? atoi(getenv("OZIMMU_SPLIT_BPS")) : 4;
+        const int64_t cap = (int64_t)num_sms * (bps > 0 ? bps : 4);
         if (k_pad >= 2048) {
-            k_split_contig<256, W, S, CPX><<<(unsigned)rows, 256, 0, st>>>(
+            const int64_t g = rows < cap ? rows : cap;
+            k_split_contig<256, W, S, CPX><<<(unsigned)g, 256, 0, st>>>(
                 M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E, vm.per_item,
                 vm.stride);
         } else {
-            k_split_contig<32, W, S, CPX><<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(
+            const int64_t nb = ceil_div(rows, 8);
+            const int64_t g = nb < 8 * cap ? nb : 8 * cap;
+            k_split_contig<32, W, S, CPX><<<(unsigned)g, 256, 0, st>>>(
                 M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E, vm.per_item,
                 vm.stride);
         }
