@@ -58,6 +58,13 @@ __host__ __device__ constexpr int nc_for(int S) {
 // s-1, ... (long and short windows alternate, so the two MMA issuers get similar work; the
 // ascending order measured the same).  The level sums are exact integers, so the order of
 // the MMAs into TMEM does not change any result.
+// L2 cache policy of the operand loads (TMA .L2::cache_hint)
+#ifndef OZ_A_HINT
+#define OZ_A_HINT ptx::kEvictNormal
+#endif
+#ifndef OZ_B_HINT
+#define OZ_B_HINT ptx::kEvictNormal
+#endif
 #ifndef OZ_KSNAKE
 #define OZ_KSNAKE 1
 #endif
@@ -278,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_arrive_expect_tx(&b_full[bs], b_tx);
                     ptx::tma_load_3d(&tmB, &b_full[bs], smB + (size_t)bs * P.b_stage_bytes,
                                      (int32_t)(kx * kKB), (int32_t)(nb * NC), 0,
-                                     ptx::kEvictNormal);
+                                     OZ_B_HINT);
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
 #pragma unroll 1
                     for (int i = 0; i < S; ++i) {
@@ -293,11 +300,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 (int32_t)(kx * kKB),
                                                 (int32_t)(mb * kBlockM + rank * (kBlockM / 2)),
                                                 slice_p(S, i) - 1,
-                                                (uint16_t)0x3, ptx::kEvictNormal);
+                                                (uint16_t)0x3, OZ_A_HINT);
                         else
                             ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
                                              (int32_t)(kx * kKB), (int32_t)(mb * kBlockM),
-                                             slice_p(S, i) - 1, ptx::kEvictNormal);
+                                             slice_p(S, i) - 1, OZ_A_HINT);
                         if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
                 }

@@ -406,10 +406,12 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
                            int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
     // kdim / k_pad count doubles of the (embedded) vector: 2 per complex element
     if (contiguous) {
-        // persistent grid of `bps` blocks per SM (OZIMMU_SPLIT_BPS, default 4): <= 148 x 4
-        // vectors of 8 k bytes in flight (77 MB at k = 16384, inside the 126 MB L2)
-        static const int bps = getenv("OZIMMU_SPLIT_BPS") ? atoi(getenv("OZIMMU_SPLIT_BPS")) : 4;
-        const int64_t cap = (int64_t)num_sms * (bps > 0 ? bps : 4);
+        // persistent grid of `bps` blocks per SM (OZIMMU_SPLIT_BPS, default 16 = as many as
+        // fit).  Capping the vectors in flight to keep pass 2 in L2 did not pay (16384^2, s = 9:
+        // 2/4/8/16 blocks per SM -> 3.53/3.31/3.24/3.21 ms for both operands): the digit
+        // extraction is issue-bound (ncu: 62% issue slots busy at 73% of DRAM bandwidth)
+        static const int bps = getenv("OZIMMU_SPLIT_BPS") ? atoi(getenv("OZIMMU_SPLIT_BPS")) : 16;
+        const int64_t cap = (int64_t)num_sms * (bps > 0 ? bps : 16);
         if (k_pad >= 2048) {
             const int64_t g = rows < cap ? rows : cap;
             k_split_contig<256, W, S, CPX><<<(unsigned)g, 256, 0, st>>>(

@@ -60,6 +60,24 @@ def test_host_pipelined_bitexact(h, ta, tb):
     assert np.array_equal(got[np.ix_(rows, cols)], ref[np.ix_(rows, cols)])
 
 
+@pytest.mark.parametrize("m,n", [(2100, 600), (520, 2600)])
+def test_host_unequal_block_counts(h, m, n):
+    """P row blocks != J column chunks (5 x 2 and 2 x 6): the alternating transfer order
+    interleaves them in proportion and every C region is computed exactly once."""
+    import torch
+    k, s = 200, 9
+    A = synth.gen_phi(m, k, 0.5, 31)
+    B = synth.gen_phi(k, n, 0.5, 32)
+    Cin = synth.gen_phi(m, n, 0.5, 33)
+    hC = _pinned(Cin)
+    h.dgemm_host("N", "N", m, n, k, 1.25, _pinned(A), m, _pinned(B), k, 0.5, hC, m, s)
+    got = np.asfortranarray(hC.numpy().reshape(n, m).T)
+    dC = dev(Cin)
+    h.dgemm("N", "N", m, n, k, 1.25, dev(A), m, dev(B), k, 0.5, dC, m, s)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, host(dC, m, n))
+
+
 @pytest.mark.parametrize("m,n,k,s", [(1, 1, 1, 3), (100, 70, 257, 9), (200, 40, 64, 14)])
 def test_host_small_full_oracle(h, m, n, k, s):
     A = synth.gen_phi(m, k, 0.5, m + 1)
