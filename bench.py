@@ -45,6 +45,8 @@ WORKLOADS = {
                 desc="C5B: batched ZGEMM, 12-qubit Haar gate on qubits 4..15 of a 28-qubit state: "
                      "batch 4096 x matmul-(16, 4096, 4096) with shared U, s=12"),
 }
+# SMs kept free of the GEMM for the NCCL broadcast of the next B chunk (N > 1)
+RESERVE_SMS = int(os.environ.get("OZIMMU_RESERVE_SMS", "8"))
 METRIC = "effective DGEMM TFLOP/s (2mnk/t) vs cuBLAS DGEMM at 1/2/4/8 B200; max rel err"
 INT8_PEAK_NOTE = ("INT8 dense peak = 2 x measured bf16 cuBLAS (nominal 4.5/2.25 POPS ratio); "
                   "'sustained' (seconds-long loop under the power cap) used: the kernel is timed "
@@ -346,6 +348,8 @@ def main():
         if one_dev:
             dist.init_process_group("gloo")
         else:
+            # the broadcast kernels run on SMs the GEMM leaves free (dist.CudaBackend)
+            os.environ.setdefault("NCCL_MAX_CTAS", str(RESERVE_SMS))
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(local)
@@ -370,7 +374,7 @@ def main():
     h.set_stream(stream)
     if s == 0:
         h.set_auto(args.auto_T, 20)
-    be = D.CudaBackend(h, dev)
+    be = D.CudaBackend(h, dev, reserve_sms=RESERVE_SMS if world > 1 else 0)
     bufs = None
 
     def step():

@@ -103,6 +103,12 @@ OZIMMU_API ozimmu_status_t ozimmu_create(ozimmu_handle_t *h, int device);
 OZIMMU_API ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h);
 /* Set the stream (a cudaStream_t passed as void*); NULL = legacy default stream. */
 OZIMMU_API ozimmu_status_t ozimmu_set_stream(ozimmu_handle_t h, void *stream);
+/* Cap the SMs the fused GEMM kernel occupies (its persistent grid; 0 = all SMs of the device).
+ * The GEMM holds one CTA of ~227 KB shared memory per SM, so a collective kernel enqueued
+ * beside it (the multi-GPU driver's NCCL broadcast of the next B chunk) can only
+ * run concurrently on SMs left free.  Results are bitwise independent of the cap.
+ * Errors: NOT_INITIALIZED, INVALID_VALUE (max_sms < 0). */
+OZIMMU_API ozimmu_status_t ozimmu_set_max_sms(ozimmu_handle_t h, int max_sms);
 /* Bytes of device workspace ozimmu_dgemm needs for this shape (0 on invalid input).
  * = s*(m + n)*round_up(k,16) INT8 planes + 4(m+n) exponents + K-chunk scratch + alignment
  * (the paper's working-memory cost). */

@@ -14,6 +14,7 @@ using namespace ozimmu;
 struct ozimmu_ctx {
     int device = 0;
     int num_sms = 148;
+    int gemm_sms = 0;  // ozimmu_set_max_sms: cap on the fused GEMM's persistent grid (0 = all)
     cudaStream_t stream = nullptr;
     void *user_ws = nullptr;
     size_t user_ws_bytes = 0;
@@ -38,6 +39,11 @@ struct ozimmu_ctx {
 namespace {
 
 constexpr size_t kAlign = 256;
+
+// SMs the fused GEMM may occupy (ozimmu_set_max_sms)
+inline int gemm_sms(ozimmu_handle_t h) {
+    return (h->gemm_sms > 0 && h->gemm_sms < h->num_sms) ? h->gemm_sms : h->num_sms;
+}
 
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -319,7 +325,7 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     const int w = slice_width(k);
     const int64_t k_pad = round_up(k, 16);
     GemmPlan gp;
-    if (!plan_gemm(s, w, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
+    if (!plan_gemm(s, w, m, n, k_pad, gemm_sms(h), &gp)) return OZIMMU_ERR_UNSUPPORTED;
     const Layout L = layout(m, bbuf_ext ? 0 : n, k_pad, s, chunk_scratch_bytes(gp, s));
     void *ws = nullptr;
     ozimmu_status_t st = get_ws(h, L.total, &ws);
@@ -491,6 +497,13 @@ ozimmu_status_t ozimmu_set_stream(ozimmu_handle_t h, void *stream) {
     return OZIMMU_SUCCESS;
 }
 
+ozimmu_status_t ozimmu_set_max_sms(ozimmu_handle_t h, int max_sms) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (max_sms < 0) return OZIMMU_ERR_INVALID_VALUE;
+    h->gemm_sms = max_sms;
+    return OZIMMU_SUCCESS;
+}
+
 size_t ozimmu_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t transB, int64_t m, int64_t n,
                               int64_t k, int num_slices) {
     if (!valid_op(transA) || !valid_op(transB) || m < 0 || n < 0 || k < 1 || num_slices < 1 ||
@@ -648,7 +661,7 @@ ozimmu_status_t ozimmu_debug_level_sums(ozimmu_handle_t h, ozimmu_op_t transA,
     const int w = slice_width(k);
     const int64_t k_pad = round_up(k, 16);
     GemmPlan gp;
-    if (!plan_gemm(s, w, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
+    if (!plan_gemm(s, w, m, n, k_pad, gemm_sms(h), &gp)) return OZIMMU_ERR_UNSUPPORTED;
     const Layout L = layout(m, n, k_pad, s, chunk_scratch_bytes(gp, s));
     void *ws = nullptr;
     if ((st = get_ws(h, L.total, &ws))) return st;
@@ -685,7 +698,7 @@ ozimmu_status_t ozimmu_debug_pair(ozimmu_handle_t h, const int8_t *Ai, const int
     if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
     const int64_t k_pad = round_up(k, 16);
     GemmPlan gp;
-    if (!plan_gemm(1, 7, m, n, k_pad, h->num_sms, &gp)) return OZIMMU_ERR_UNSUPPORTED;
+    if (!plan_gemm(1, 7, m, n, k_pad, gemm_sms(h), &gp)) return OZIMMU_ERR_UNSUPPORTED;
     gp.chunk_blocks = gp.num_k_blocks;  // caller guarantees the INT32 budget
     gp.k_chunks = 1;
     gp.T = 1;
@@ -748,7 +761,7 @@ static ozimmu_status_t zgemm_core(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_
     const int64_t k_pad = round_up(K2, 16);
     GemmPlan gp;
     Layout L;
-    if (!zgemm_ws(m, n, k, s, h->num_sms, &gp, &L)) return OZIMMU_ERR_UNSUPPORTED;
+    if (!zgemm_ws(m, n, k, s, gemm_sms(h), &gp, &L)) return OZIMMU_ERR_UNSUPPORTED;
     void *ws = nullptr;
     if ((st = get_ws(h, L.total, &ws))) return st;
     uint8_t *base = static_cast<uint8_t *>(ws);
@@ -998,7 +1011,7 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     const int64_t shapes[3][2] = {{mb, nb}, {m, nb}, {mb, n}};
     for (auto &sh : shapes) {
         GemmPlan gp;
-        if (!plan_gemm(s, w, sh[0], sh[1], k_pad, h->num_sms, &gp)) return false;
+        if (!plan_gemm(s, w, sh[0], sh[1], k_pad, gemm_sms(h), &gp)) return false;
         const size_t c = chunk_scratch_bytes(gp, s);
         if (c > scratch) scratch = c;
     }
@@ -1162,7 +1175,7 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
             OZ_TRY(cudaStreamWaitEvent(cs, ev_cin[q], 0));
         }
         GemmPlan gp;
-        if (!plan_gemm(s, w, mr, nc, k_pad, h->num_sms, &gp)) {
+        if (!plan_gemm(s, w, mr, nc, k_pad, gemm_sms(h), &gp)) {
             if (e == cudaSuccess) e = cudaErrorInvalidValue;
             return;
         }
@@ -1223,7 +1236,7 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     free(ev);
     if (e != cudaSuccess) return cuda_status(e);
     GemmPlan gp;
-    plan_gemm(s, w, hp.mb, n, k_pad, h->num_sms, &gp);
+    plan_gemm(s, w, hp.mb, n, k_pad, gemm_sms(h), &gp);
     fill_report(h, s, w, m, n, k, &gp, launches, (int64_t)s * (m + n) * k_pad + 4 * (m + n));
     return OZIMMU_SUCCESS;
 }

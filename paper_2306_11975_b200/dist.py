@@ -30,11 +30,25 @@ def col_chunks(n, chunk_cols):
 
 
 class CudaBackend:
-    """Backend over libozimmu (device pointers, column-major, stream = current)."""
+    """Backend over libozimmu (device pointers, column-major, stream = current).
 
-    def __init__(self, handle, device):
+    reserve_sms: SMs kept free of the fused GEMM while broadcasts are in flight.  The GEMM
+    is a persistent kernel with one ~227 KB-shared-memory CTA per SM, so an NCCL kernel
+    enqueued beside it only runs on SMs it leaves free; without a reserve the broadcast of
+    chunk c+1 would wait for the GEMM of chunk c instead of overlapping it.  Pair it with
+    NCCL_MAX_CTAS <= reserve_sms (bench.py does)."""
+
+    def __init__(self, handle, device, reserve_sms=0):
         self.h = handle
         self.device = torch.device("cuda", device) if isinstance(device, int) else device
+        self.reserve_sms = int(reserve_sms)
+
+    def overlap(self, on):
+        """GEMMs leave `reserve_sms` SMs free while `on` (broadcasts in flight)."""
+        if self.reserve_sms <= 0:
+            return
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        self.h.set_max_sms(max(1, sms - self.reserve_sms) if on else 0)
 
     def b_slices_bytes(self, n, k, s):
         from .ozimmu import b_slices_bytes
@@ -78,9 +92,15 @@ def dgemm_rowblock(backend, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, l
             works.append(dist.broadcast(buf, src=root, group=group, async_op=True))
         else:
             works.append(None)
-    for (c0, c1), buf, w in zip(chunks, bufs, works):
+    overlap = getattr(backend, "overlap", None)
+    last = len(chunks) - 1
+    for i, ((c0, c1), buf, w) in enumerate(zip(chunks, bufs, works)):
         if w is not None:
             w.wait()  # NCCL: the current stream waits for this chunk only
+        if overlap is not None and world > 1:
+            overlap(i < last)  # later chunks still in flight: leave SMs to NCCL
         if m_loc > 0:
             backend.gemm(transA, m_loc, c0, c1, k, alpha, A_loc, lda, buf, beta, C_loc, ldc, s)
+    if overlap is not None and world > 1:
+        overlap(False)
     return bufs

@@ -29,7 +29,7 @@ EXPORTS = [
     "ozimmu_debug_split", "ozimmu_debug_level_sums", "ozimmu_debug_pair",
     "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
     "ozimmu_set_auto", "ozimmu_auto_splits", "ozimmu_dgemm_strided_batched",
-    "ozimmu_zgemm_strided_batched", "ozimmu_dgemm_host",
+    "ozimmu_zgemm_strided_batched", "ozimmu_dgemm_host", "ozimmu_set_max_sms",
 ]
 
 
@@ -72,6 +72,7 @@ def lib():
         "ozimmu_create": ([ct.POINTER(H), i32], i32),
         "ozimmu_destroy": ([H], i32),
         "ozimmu_set_stream": ([H, vp], i32),
+        "ozimmu_set_max_sms": ([H, i32], i32),
         "ozimmu_workspace_bytes": ([i32, i32, i64, i64, i64, i32], sz),
         "ozimmu_set_workspace": ([H, vp, sz], i32),
         "ozimmu_get_report": ([H, ct.POINTER(Report)], i32),
@@ -170,6 +171,10 @@ class Handle:
         """stream: torch.cuda.Stream, raw cudaStream_t int, or None (legacy default)."""
         raw = None if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
         _check("ozimmu_set_stream", lib().ozimmu_set_stream(self._h, raw))
+
+    def set_max_sms(self, max_sms):
+        """Cap the SMs of the fused GEMM's persistent grid (0 = all); see ozimmu_set_max_sms."""
+        _check("ozimmu_set_max_sms", lib().ozimmu_set_max_sms(self._h, int(max_sms)))
 
     def set_workspace(self, tensor_or_ptr, nbytes=None):
         if tensor_or_ptr is None:

@@ -56,7 +56,7 @@ def _worker(rank, world, port, cfg, q):
         dC = torch.from_numpy(C_loc.ravel(order="F").copy()).to(dev)
         h = oz.Handle(0)
         h.set_stream(torch.cuda.current_stream(dev))
-        be = D.CudaBackend(h, dev)
+        be = D.CudaBackend(h, dev, reserve_sms=21)  # capped GEMM grid (127 SMs) while in flight
         D.dgemm_rowblock(be, ta, tb, ml, n, k, 1.5, dA, lda, dB, B.shape[0], -0.5,
                          dC, max(1, ml), s, root=root, chunk_cols=chunk)
         torch.cuda.synchronize()
