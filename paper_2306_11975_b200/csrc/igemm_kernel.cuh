@@ -23,10 +23,11 @@ struct KParams {
     int64_t num_k_blocks, chunk_blocks;
     int k_chunks;
     int64_t tiles_m, tiles_n, num_tiles;
-    // work units: cl = 1 -> one tile per unit; cl = 2 -> a cluster of two CTAs takes the
-    // column tiles (2 j, 2 j + 1) of one row block, the A tiles multicast to both
-    int cl;
-    int64_t units_n, num_units;
+    // work units: one per cluster of cl = clm x cln CTAs, which takes row blocks
+    // (clm i .. clm i + clm-1) x column tiles (cln j .. cln j + cln-1); the CTAs of a row
+    // block share its A tiles (TMA multicast), the CTAs of a column tile share its B tiles
+    int cl, clm, cln;
+    int64_t units_m, units_n, num_units;
     int a_stages, b_stages;
     uint32_t a_stage_bytes, b_stage_bytes;
     uint32_t tmem_cols;
@@ -80,17 +81,20 @@ enum : int { ST_TOTAL = 0, ST_MMA_WAIT_B, ST_MMA_WAIT_A, ST_MMA_WAIT_TMEM, ST_PR
              ST_PROD_WAIT_A, ST_PROD_WAIT_B, ST_EPI_BUSY, ST_EPI_TMEM, ST_EPI_STORE,
              ST_MMA_FIRST_A, ST_MMA_B_TILE0, kStatSlots = 12 };
 
-// Grouped raster over units (kGroupM row blocks per group); rank = CTA rank in the cluster.
+// Grouped raster over units (kGroupM row blocks per group); rank = CTA rank in the cluster
+// (rank = rm * cln + rn).  mb / nb may reach tiles_m / tiles_n: a dummy tile (operands
+// zero-filled by TMA, no stores).
 __device__ __forceinline__ void tile_coords(int64_t u, const KParams &P, uint32_t rank,
                                             int64_t &mb, int64_t &nb) {
-    const int64_t per_group = (int64_t)kGroupM * P.units_n;
+    const int64_t GM = kGroupM / P.clm;  // unit rows per group
+    const int64_t per_group = GM * P.units_n;
     const int64_t g = u / per_group;
     const int64_t r = u % per_group;
-    const int64_t gm0 = g * kGroupM;
-    int64_t gsz = P.tiles_m - gm0;
-    gsz = gsz < kGroupM ? gsz : kGroupM;
-    mb = gm0 + r % gsz;
-    nb = (r / gsz) * P.cl + rank;  // cl = 2: nb may reach tiles_n (a dummy tile, no stores)
+    const int64_t gm0 = g * GM;
+    int64_t gsz = P.units_m - gm0;
+    gsz = gsz < GM ? gsz : GM;
+    mb = (gm0 + r % gsz) * P.clm + (int64_t)(rank / (uint32_t)P.cln);
+    nb = (r / gsz) * P.cln + (int64_t)(rank % (uint32_t)P.cln);
 }
 
 // 2^e as a double for e in the normal range (exact).
@@ -214,16 +218,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
     constexpr int s = S;
-    const uint32_t rank = P.cl == 2 ? ptx::cluster_ctarank() : 0u;
+    const uint32_t rank = P.cl > 1 ? ptx::cluster_ctarank() : 0u;
+    const uint32_t rm = rank / (uint32_t)P.cln, rn = rank % (uint32_t)P.cln;
+    // multicast groups: CTAs sharing this CTA's row block (A) / column tile (B)
+    const uint16_t amask = (uint16_t)(((1u << P.cln) - 1u) << (rm * P.cln));
+    uint16_t bmask = 0;
+    for (int j = 0; j < P.clm; ++j) bmask |= (uint16_t)(1u << (j * P.cln + rn));
 
     if (warp == 5 && lane == 0) {
         for (int i = 0; i < P.b_stages; ++i) {
             ptx::mbar_init(&b_full[i], 1);
-            ptx::mbar_init(&b_empty[i], 2);  // released by both MMA issuers
+            ptx::mbar_init(&b_empty[i], 2 * P.clm);  // both MMA issuers of each CTA sharing it
         }
         for (int i = 0; i < P.a_stages; ++i) {
             ptx::mbar_init(&a_full[i], 1);
-            ptx::mbar_init(&a_empty[i], (uint32_t)P.cl);  // released by both CTAs' MMAs
+            ptx::mbar_init(&a_empty[i], (uint32_t)P.cln);  // the MMAs of each CTA sharing it
         }
         ptx::mbar_init(tmem_full, 2);  // committed by both MMA issuers
         ptx::mbar_init(tmem_empty, 4 * 32);
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tmem_relinquish();
     }
     ptx::tc_fence_before();
-    if (P.cl == 2) ptx::cluster_sync();  // peers' barriers initialised before any multicast
+    if (P.cl > 1) ptx::cluster_sync();  // peers' barriers initialised before any multicast
     else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
@@ -283,9 +292,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&b_empty[bs], bph ^ 1);
                     if (P.stats) st_pb += clock64() - c1;
                     ptx::mbar_arrive_expect_tx(&b_full[bs], b_tx);
-                    ptx::tma_load_3d(&tmB, &b_full[bs], smB + (size_t)bs * P.b_stage_bytes,
-                                     (int32_t)(kx * kKB), (int32_t)(nb * NC), 0,
-                                     OZ_B_HINT);
+                    if (P.clm == 1) {
+                        ptx::tma_load_3d(&tmB, &b_full[bs], smB + (size_t)bs * P.b_stage_bytes,
+                                         (int32_t)(kx * kKB), (int32_t)(nb * NC), 0, OZ_B_HINT);
+                    } else {  // this CTA's NC/clm columns of every slice, to its column group
+                        const int part = NC / P.clm;
+#pragma unroll 1
+                        for (int z = 0; z < S; ++z)
+                            ptx::tma_load_3d_mc(&tmB, &b_full[bs],
+                                                smB + (size_t)bs * P.b_stage_bytes +
+                                                    (size_t)(z * NC + (int)rm * part) * kKB,
+                                                (int32_t)(kx * kKB),
+                                                (int32_t)(nb * NC + (int)rm * part), z, bmask,
+                                                OZ_B_HINT);
+                    }
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
 #pragma unroll 1
                     for (int i = 0; i < S; ++i) {
@@ -293,14 +313,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mbar_wait(&a_empty[as], aph ^ 1);
                         if (P.stats) st_pa += clock64() - c2;
                         ptx::mbar_arrive_expect_tx(&a_full[as], a_tx);
-                        if (P.cl == 2)  // this CTA's half of the rows, to both CTAs
+                        if (P.cln > 1) {  // this CTA's rows of the tile, to its row group
+                            const int part = kBlockM / P.cln;
                             ptx::tma_load_3d_mc(&tmA, &a_full[as],
                                                 smA + (size_t)as * P.a_stage_bytes +
-                                                    rank * (kBlockM / 2) * kKB,
+                                                    (size_t)rn * part * kKB,
                                                 (int32_t)(kx * kKB),
-                                                (int32_t)(mb * kBlockM + rank * (kBlockM / 2)),
-                                                slice_p(S, i) - 1,
-                                                (uint16_t)0x3, OZ_A_HINT);
+                                                (int32_t)(mb * kBlockM + (int)rn * part),
+                                                slice_p(S, i) - 1, amask, OZ_A_HINT);
+                        }
                         else
                             ptx::tma_load_3d(&tmA, &a_full[as], smA + (size_t)as * P.a_stage_bytes,
                                              (int32_t)(kx * kKB), (int32_t)(mb * kBlockM),
@@ -309,12 +330,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (P.cl == 2) {
-                // drain: every A slot released by both CTAs, so no multicast arrive is still
-                // in flight towards this CTA when the cluster exits
+            if (P.cl > 1) {
+                // drain: every slot released by all CTAs sharing it, so no multicast arrive
+                // is still in flight towards a peer when the cluster exits
                 for (int i = 0; i < P.a_stages; ++i) {
                     ptx::mbar_wait(&a_empty[as], aph ^ 1);
                     if (++as == P.a_stages) { as = 0; aph ^= 1; }
+                }
+                for (int i = 0; i < P.b_stages; ++i) {
+                    ptx::mbar_wait(&b_empty[bs], bph ^ 1);
+                    if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
                 }
             }
             if (P.stats) {
@@ -401,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 for (int ks = 0; ks < kKB / 32; ++ks)
                                     issue(p, adesc0 + (uint64_t)(ks * 2),
                                           bdesc0 + (uint64_t)(((p - 1) * NC * kKB + ks * 32) >> 4));
-                                if (P.cl == 2) ptx::mma_commit_mc(&a_empty[as], (uint16_t)0x3);
+                                if (P.cln > 1) ptx::mma_commit_mc(&a_empty[as], amask);
                                 else ptx::mma_commit(&a_empty[as]);
                             }
                             __syncwarp();
@@ -409,7 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (++as == P.a_stages) { as = 0; aph ^= 1; }
                     }
                     tpar += (uint32_t)S;
-                    if (ptx::elect_one()) ptx::mma_commit(&b_empty[bs]);
+                    if (ptx::elect_one()) {
+                        if (P.clm > 1) ptx::mma_commit_mc(&b_empty[bs], bmask);
+                        else ptx::mma_commit(&b_empty[bs]);
+                    }
                     __syncwarp();
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
                 }
@@ -608,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             P.stats[(int64_t)blockIdx.x * kStatSlots + ST_EPI_STORE] = st_es;
         }
     }
-    if (P.cl == 2) ptx::cluster_sync();
+    if (P.cl > 1) ptx::cluster_sync();
     else __syncthreads();
     if (warp == 0) {
         ptx::tc_fence_after();
@@ -669,29 +697,35 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     // larger operand stream: 128 rows x s slices per k-block vs NC x s for B).  Measured at
     // 16384^3, s = 9: +1.7% (less L2 traffic -> more clock under the power cap).  Pairs take
     // column tiles (2j, 2j+1); an odd column-tile count leaves one dummy tile per row block,
-    // so pairs are used only when that waste is small.  OZIMMU_CLUSTER=1 forces single CTAs.
+    // so pairs are used only when that waste is small.  OZIMMU_CLUSTER=1 forces single CTAs;
+    // OZIMMU_CLUSTER=4 takes 2 x 2 clusters (B tiles multicast down the row-block pair too).
 #ifndef OZ_CLUSTER_DEFAULT
 #define OZ_CLUSTER_DEFAULT 2
 #endif
     static const int cl_env =
         getenv("OZIMMU_CLUSTER") ? atoi(getenv("OZIMMU_CLUSTER")) : OZ_CLUSTER_DEFAULT;
     const int64_t tiles_m = ceil_div(a.m, kBlockM), tiles_n = ceil_div(a.n, NC);
-    int cl = (cl_env == 2 && tiles_n >= 2 && (tiles_n % 2 == 0 || tiles_n >= 32) && p.grid >= 2)
-                 ? 2 : 1;
+    // a dimension is split over the cluster only when the dummy tiles it leaves are few
+    auto splits = [](int64_t tiles) { return tiles >= 2 && (tiles % 2 == 0 || tiles >= 32); };
+    int clm = 1, cln = 1;
+    if (cl_env >= 2 && splits(tiles_n)) cln = 2;
+    if (cl_env >= 4 && cln == 2 && splits(tiles_m)) clm = 2;
+    int cl = clm * cln;
+    if (p.grid < cl) clm = cln = cl = 1;
     int grid = p.grid;
     cudaLaunchAttribute attr[1];
-    if (cl == 2) {
+    if (cl > 1) {
         int dev = 0;
         cudaGetDevice(&dev);
-        static int maxc_cache[64][33];
-        int &maxc = maxc_cache[dev & 63][S];
+        static int maxc_cache[64][33][5];
+        int &maxc = maxc_cache[dev & 63][S][cl];
         if (maxc == 0) {
             cudaLaunchConfig_t q = {};
-            q.gridDim = dim3((unsigned)(p.grid & ~1));
+            q.gridDim = dim3((unsigned)(p.grid / cl * cl));
             q.blockDim = dim3(kThreads);
             q.dynamicSmemBytes = p.smem_bytes;
             attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.x = cl;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             q.attrs = attr;
@@ -701,20 +735,22 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
                 maxc = -1;
             }
         }
-        const int64_t units = tiles_m * ceil_div(tiles_n, 2);
+        const int64_t units = ceil_div(tiles_m, clm) * ceil_div(tiles_n, cln);
         if (maxc < 1) {
-            cl = 1;
+            clm = cln = cl = 1;
         } else {
-            int64_t c = maxc < p.grid / 2 ? maxc : p.grid / 2;
+            int64_t c = maxc < p.grid / cl ? maxc : p.grid / cl;
             c = c < units ? c : units;
-            grid = (int)(2 * c);
+            grid = (int)(cl * c);
         }
     }
     CUtensorMap tmA, tmB;
-    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, cl == 2 ? kBlockM / 2 : kBlockM, 1,
+    if (!make_map(&tmA, a.a_planes, a.k_pad, a.m, a.s, (uint32_t)(kBlockM / cln), 1,
                   a.a_plane_rows))
         return cudaErrorInvalidValue;
-    if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, NC, (uint32_t)a.s, a.b_plane_rows))
+    // B: one box of all s slices, or (clm > 1) one box of NC/clm columns per slice
+    if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, (uint32_t)(NC / clm),
+                  clm == 1 ? (uint32_t)a.s : 1u, a.b_plane_rows))
         return cudaErrorInvalidValue;
     CUtensorMap tmApf;  // up to 8 A-slice tiles of a k-block per box (L2 prefetch only)
     if (!make_map(&tmApf, a.a_planes, a.k_pad, a.m, a.s, kBlockM, (uint32_t)(a.s < 8 ? a.s : 8),
@@ -758,8 +794,11 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.region_col[0] = 0;
     P.region_col[1] = (uint32_t)(S * NC);
     P.cl = cl;
-    P.units_n = cl == 2 ? ceil_div(P.tiles_n, 2) : P.tiles_n;
-    P.num_units = P.tiles_m * P.units_n;
+    P.clm = clm;
+    P.cln = cln;
+    P.units_m = ceil_div(P.tiles_m, clm);
+    P.units_n = ceil_div(P.tiles_n, cln);
+    P.num_units = P.units_m * P.units_n;
     P.full_waves = P.num_units / (grid / cl);
     if (P.wave_counter) {
         e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
@@ -775,7 +814,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;

@@ -1,8 +1,9 @@
 """The fused GEMM runs by default as CTA pairs (clusters of two CTAs, A tiles TMA-multicast
 to both, dummy tile when the column-tile count is odd); OZIMMU_CLUSTER=1 forces single CTAs.
-Both must give the same bits: the default suites cover the pairs, this re-runs the DGEMM /
-ZGEMM / batched parity suites with single CTAs (the variable is read once per process,
-hence the subprocess)."""
+OZIMMU_CLUSTER=4 takes 2 x 2 clusters (B tiles multicast between the two row blocks too).
+All must give the same bits: the default suites cover the pairs, this re-runs the DGEMM /
+ZGEMM / batched parity suites with single CTAs and with 2 x 2 clusters (the variable is read
+once per process, hence the subprocess)."""
 import os
 import subprocess
 import sys
@@ -14,8 +15,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_parity_suites_with_single_ctas():
-    env = dict(os.environ, OZIMMU_CLUSTER="1")
+@pytest.mark.parametrize("cl", ["1", "4"])
+def test_parity_suites_with_other_cluster_shapes(cl):
+    env = dict(os.environ, OZIMMU_CLUSTER=cl)
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
                         os.path.join(ROOT, "tests", "test_gpu_parity.py"),
                         os.path.join(ROOT, "tests", "test_gpu_zgemm.py"),
