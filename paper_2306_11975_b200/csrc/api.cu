@@ -2,6 +2,7 @@
 // workspace, and the launch sequence  slice(A) -> slice(B) -> fused tcgen05 GEMM+epilogue.
 #include <cstdint>
 #include <cstdlib>
+#include <vector>
 #include <cstring>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -987,6 +988,7 @@ namespace {
 // ld m) and the GEMM scratch.
 struct HostPlan {
     int64_t mb, nb, P, J;
+    std::vector<int64_t> rb, cb;  // row-block / column-chunk boundaries (P+1 / J+1 entries)
     size_t o_apl, o_bbuf, o_ast[2], o_bst[2], o_c, o_keys, o_sync, o_scratch, total;
 };
 
@@ -1005,8 +1007,29 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     if (nb > n) nb = n;
     hp->mb = mb;
     hp->nb = nb;
-    hp->P = ceil_div(m, mb);
-    hp->J = ceil_div(n, nb);
+    // the first and the last block are half-size: the first GEMM waits for less H2D, the
+    // last region's D2H (the drain after the last GEMM) moves less
+    auto bounds = [](int64_t total, int64_t blk, int64_t align, std::vector<int64_t> &b) {
+        b.assign(1, 0);
+        int64_t half = round_up(blk / 2, align);
+        if (half >= blk || total <= blk) {  // no halving: equal blocks
+            for (int64_t x = blk; x < total; x += blk) b.push_back(x);
+            b.push_back(total);
+            return;
+        }
+        int64_t x = half;
+        b.push_back(x);
+        while (total - x > blk + half) {
+            x += blk;
+            b.push_back(x);
+        }
+        if (total - x > half) b.push_back(total - half);
+        b.push_back(total);
+    };
+    bounds(m, mb, 128, hp->rb);
+    bounds(n, nb, 96, hp->cb);
+    hp->P = (int64_t)hp->rb.size() - 1;
+    hp->J = (int64_t)hp->cb.size() - 1;
     size_t scratch = 0;
     const int64_t shapes[3][2] = {{mb, nb}, {m, nb}, {mb, n}};
     for (auto &sh : shapes) {
@@ -1162,8 +1185,8 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_start, 0));
     OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_start, 0));
 
-    auto rows_of = [&](int64_t i) { return (i == P - 1) ? m - i * hp.mb : hp.mb; };
-    auto cols_of = [&](int64_t j) { return (j == J - 1) ? n - j * hp.nb : hp.nb; };
+    auto rows_of = [&](int64_t i) { return hp.rb[i + 1] - hp.rb[i]; };
+    auto cols_of = [&](int64_t j) { return hp.cb[j + 1] - hp.cb[j]; };
     // C region rows [r0, r0+mr) x cols [c0, c0+nc): (beta C in), GEMM, C out
     auto region = [&](int64_t r0, int64_t mr, int64_t c0, int64_t nc) {
         if (mr <= 0 || nc <= 0) return;
@@ -1191,7 +1214,7 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     while (ia < P || jb < J) {
         const bool take_a = ia < P && (jb >= J || ia * J <= jb * P);
         if (take_a) {
-            const int64_t i = ia, r0 = i * hp.mb, mi = rows_of(i);
+            const int64_t i = ia, r0 = hp.rb[i], mi = rows_of(i);
             double *dst = reinterpret_cast<double *>(base + hp.o_ast[i & 1]);
             if (i >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_afree[i - 2], 0));
             if (a_rows_contig)  // stored k x m: columns r0 .. r0+mi
@@ -1205,9 +1228,9 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
                                 keys, h->num_sms, cs, &launches));
             OZ_TRY(cudaEventRecord(ev_afree[i], cs));
             ++ia;
-            region(r0, mi, 0, jb == J ? n : jb * hp.nb);
+            region(r0, mi, 0, hp.cb[jb]);
         } else {
-            const int64_t j = jb, c0 = j * hp.nb, nc = cols_of(j);
+            const int64_t j = jb, c0 = hp.cb[j], nc = cols_of(j);
             double *dst = reinterpret_cast<double *>(base + hp.o_bst[j & 1]);
             if (j >= 2) OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_bfree[j - 2], 0));
             if (b_cols_contig)  // stored k x n: columns c0 .. c0+nc
@@ -1221,7 +1244,7 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
                                 h->num_sms, cs, &launches));
             OZ_TRY(cudaEventRecord(ev_bfree[j], cs));
             ++jb;
-            region(0, ia == P ? m : ia * hp.mb, c0, nc);
+            region(0, hp.rb[ia], c0, nc);
         }
     }
     for (int64_t q = 0; q < nreg; ++q) OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[q], 0));

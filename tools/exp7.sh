@@ -1,4 +1,4 @@
-for cfg in "1024 1056" "2048 2112" "4096 4128"; do
+for cfg in "1024 1056" "512 576" "2048 2112"; do
   set -- $cfg
   OZIMMU_HOST_MB=$1 OZIMMU_HOST_NB=$2 timeout 300 python - >> gpurun_out/exp7_host.log 2>&1 <<'PY'
 import os, sys, time, json
