@@ -6,7 +6,10 @@
 //
 // Design:
 //  * Output tile = 128 rows x NC columns of C, one CTA per SM (persistent, grouped raster,
-//    soft per-wave grid barrier so CTAs sharing operands stream K through L2 together).
+//    soft per-wave grid barrier so CTAs sharing operands stream K through L2 together, odd
+//    waves walking K backwards), CTAs in clusters of two sharing A tiles by TMA multicast.
+//  * Warp roles: 4 epilogue warps, 1 TMA producer, 2 MMA issuers taking alternate A-slice
+//    tiles (one issuer leaves the tensor pipe idle during its per-tile barrier wait).
 //  * K is processed in k-blocks of 128 bytes (one 128B-swizzle row).  Per k-block ONE 3-D
 //    TMA box brings all s B-slice tiles of the NC columns (B planes are stored in reversed
 //    slice order q -> s-q) into the B ring, and the s A-slice tiles (128 x 128 B each) flow
@@ -17,9 +20,10 @@
 //    and window block j lands in TMEM column block j, which always holds level g = s+1-j.
 //    So TMEM accumulates the exact per-level sums L_g directly: each A and B slice tile
 //    is loaded once per k-block and every pair i+j <= s+1 is covered.
-//  * INT32 budget: a level has <= s pairs, so K is processed in chunks with
-//    s * k_chunk * (2^w-1)^2 <= 2^31-1; between chunks the epilogue drains TMEM into exact
-//    int64 partial sums (per-CTA global scratch).
+//  * INT32 budget: a level has <= s pairs; when s * k * (2^w-1)^2 > 2^31-1 the
+//    pairs of the top levels go to a second TMEM region (T = 2), else K is processed in
+//    chunks and between chunks the epilogue drains TMEM into exact int64 partial sums
+//    (per-CTA global scratch).  MMAs only accumulate: the epilogue zeroes what it read.
 //  * Epilogue (4 warps, TMEM lane quarter = warp % 4): L_g -> FP64 in the canonical
 //    order g = s+1 .. 2 (reading A6), ldexp by E_A+E_B (A7), alpha/beta (A8), NaN rows (A9),
 //    coalesced column-major stores of C.
