@@ -199,7 +199,7 @@ def run_reference(args, wl):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "i8", "data": "synthetic",
-            "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "batch": batch, "phi": wl["phi"],
+            "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "phi": wl["phi"],
                        "parallelism": "cpu oracle, OpenMP"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores,
                              "kind": "oracle", "sample": sample},

@@ -113,6 +113,109 @@ __device__ __forceinline__ void store_digits(const Digits<W, S> (&dg)[8], int s,
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Fast path for W * S <= 64 (s <= 9 at w = 7): the whole fraction window of an element is
+// one 64-bit word V = floor(|x| 2^(64 - E)) (one variable shift of the significand), digit
+// p is bits [64 - W p, 64 - W (p-1)) of V, and the signs are applied four digits at a time
+// on the packed bytes: for a byte d in [0, 127], -d = (0x80 - d) ^ 0x80 (no borrow leaves
+// the byte), selected by a per-byte mask of the negative elements.
+// ---------------------------------------------------------------------------------
+template <int W, int S>
+struct Chunk64 {
+    static_assert(W * S <= 64, "fraction window must fit 64 bits");
+    uint64_t V[8];
+    uint32_t neg[2];  // 0xFF per byte of a negative element (elements 0-3, 4-7)
+
+    // x[] finite, |x| < 2^E (zeros give V = 0)
+    __device__ __forceinline__ void init(const double (&x)[8], int32_t E) {
+        neg[0] = neg[1] = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x[i]));
+            const int be = static_cast<int>((u >> 52) & 0x7FF);
+            const uint64_t fr = u & ((1ull << 52) - 1);
+            const uint64_t M = be ? (fr | (1ull << 52)) : fr;  // |x| = M 2^e0
+            const int e0 = be ? be - 1075 : -1074;
+            const int sh = e0 - E + 64;  // V = floor(M 2^sh), sh <= 11 since |x| < 2^E
+            V[i] = sh >= 0 ? (M << sh) : (-sh < 64 ? (M >> -sh) : 0ull);
+            neg[i >> 2] |= (static_cast<uint32_t>(u >> 63) * 0xFFu) << (8 * (i & 3));
+        }
+    }
+    // magnitudes of digit P of elements e0 .. e0+3, one per byte
+    template <int P>
+    __device__ __forceinline__ uint32_t mags(int e0) const {
+        constexpr int sh = 64 - W * P;
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            w |= (static_cast<uint32_t>(V[e0 + e] >> sh) & ((1u << W) - 1)) << (8 * e);
+        return w;
+    }
+    // swapped pairs (element 2j <-> 2j+1): magnitudes of V[e ^ 1]
+    template <int P>
+    __device__ __forceinline__ uint32_t mags_swapped(int e0) const {
+        constexpr int sh = 64 - W * P;
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            w |= (static_cast<uint32_t>(V[(e0 + e) ^ 1] >> sh) & ((1u << W) - 1)) << (8 * e);
+        return w;
+    }
+};
+
+__device__ __forceinline__ uint32_t apply_signs(uint32_t w, uint32_t m) {
+    const uint32_t n = (0x80808080u - w) ^ 0x80808080u;
+    return w ^ ((w ^ n) & m);
+}
+
+// digit planes p = 1..s of the 8 elements: one 8-byte store per plane; `m` = sign masks
+template <int W, int S, bool SWAP, int P = 1>
+__device__ __forceinline__ void store_planes64(const Chunk64<W, S> &c, uint32_t m0, uint32_t m1,
+                                               int s, int reverse, int8_t *dst,
+                                               int64_t plane_stride) {
+    if constexpr (P <= S) {
+        if (P <= s) {
+            uint2 v;
+            if constexpr (SWAP) {
+                v.x = apply_signs(c.template mags_swapped<P>(0), m0);
+                v.y = apply_signs(c.template mags_swapped<P>(4), m1);
+            } else {
+                v.x = apply_signs(c.template mags<P>(0), m0);
+                v.y = apply_signs(c.template mags<P>(4), m1);
+            }
+            const int pidx = reverse ? (s - P) : (P - 1);
+            *reinterpret_cast<uint2 *>(dst + pidx * plane_stride) = v;
+            store_planes64<W, S, SWAP, P + 1>(c, m0, m1, s, reverse, dst, plane_stride);
+        }
+    }
+}
+
+// emit() for Chunk64 (same three operand forms, same signs as below)
+template <int W, int S, int CPX>
+__device__ __forceinline__ void emit64(const Chunk64<W, S> &c, int s, int reverse, int conj,
+                                       int8_t *planes, int64_t r, int64_t l0, int64_t k_pad,
+                                       int64_t plane_stride) {
+    constexpr uint32_t kOdd = 0xFF00FF00u, kEven = 0x00FF00FFu;
+    if constexpr (CPX == 0) {
+        store_planes64<W, S, false>(c, c.neg[0], c.neg[1], s, reverse, planes + r * k_pad + l0,
+                                    plane_stride);
+    } else if constexpr (CPX == 1) {
+        const uint32_t f = conj ? kOdd : 0u;  // conj: Im negated
+        store_planes64<W, S, false>(c, c.neg[0] ^ f, c.neg[1] ^ f, s, reverse,
+                                    planes + r * k_pad + l0, plane_stride);
+    } else {
+        // row 2r = (Re, -Im) (Im := -Im if conj); row 2r+1 = (Im, Re) with the (re, im)
+        // swap applied to the masks too
+        const uint32_t f0 = conj ? 0u : kOdd;
+        store_planes64<W, S, false>(c, c.neg[0] ^ f0, c.neg[1] ^ f0, s, reverse,
+                                    planes + (2 * r) * k_pad + l0, plane_stride);
+        auto swapb = [](uint32_t m) { return __byte_perm(m, 0, 0x2301); };
+        const uint32_t f1 = conj ? kEven : 0u;
+        store_planes64<W, S, true>(c, swapb(c.neg[0]) ^ f1, swapb(c.neg[1]) ^ f1, s, reverse,
+                                   planes + (2 * r + 1) * k_pad + l0, plane_stride);
+    }
+}
+
 // Output of one 8-element chunk (elements l0..l0+7 of input vector r) for the three
 // operand forms (ZGEMM reading A16, real embedding with interleaved K):
 //   CPX 0  real vector                    -> row r
@@ -228,10 +331,20 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
             const int64_t l0 = c * 8;
             double x[8];
             if (!bad) load8(v, l0, kdim, al16, x);
-            Digits<W, S> dg[8];
+            if constexpr (W * S <= 64) {
+                if (bad) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-            emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
+                    for (int i = 0; i < 8; ++i) x[i] = 0.0;
+                }
+                Chunk64<W, S> c;
+                c.init(x, bad ? 0 : Ev);
+                emit64<W, S, CPX>(c, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
+            } else {
+                Digits<W, S> dg[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
+                emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
+            }
         }
     }
 }
@@ -365,10 +478,20 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
             x[2 * h] = d2.x;
             x[2 * h + 1] = d2.y;
         }
-        Digits<W, S> dg[8];
+        if constexpr (W * S <= 64) {
+            if (bad) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-        emit<W, S, CPX>(dg, s, reverse, conj, planes, r, lb, k_pad, plane_stride);
+                for (int i = 0; i < 8; ++i) x[i] = 0.0;
+            }
+            Chunk64<W, S> c;
+            c.init(x, bad ? 0 : Ev);
+            emit64<W, S, CPX>(c, s, reverse, conj, planes, r, lb, k_pad, plane_stride);
+        } else {
+            Digits<W, S> dg[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
+            emit<W, S, CPX>(dg, s, reverse, conj, planes, r, lb, k_pad, plane_stride);
+        }
     }
 }
 

@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/exp15_tests.log 2>&1
+for i in 1 2; do timeout 300 python bench.py --steps 5 --no-e2e --no-cpu-baseline --no-cublas > gpurun_out/exp15_bench$i.log 2>&1; done
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active
+timeout 300 ncu --kernel-name regex:k_split --launch-skip 2 --launch-count 2 --clock-control none --metrics $M --csv python tools/stats_run.py 16384 9 > gpurun_out/exp15_ncu_split.csv 2>&1
