@@ -58,6 +58,10 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     int a_stages = (int)((smem_budget - b_stages * b_stage) / a_stage);
     if (a_stages > 12) a_stages = 12;
     if (as_env && atoi(as_env) >= 2 && atoi(as_env) < a_stages) a_stages = atoi(as_env);
+    // even: the two MMA issuer warps take alternate A tiles, so with an even ring every slot
+    // always belongs to the same warp (k_oz_gemm's parity waits rely on it)
+    a_stages &= ~1;
+    if (a_stages < 2) return false;
     // INT32 budget: an accumulator holding `g` pair products over K' values of k
     // needs g * K' * (2^w - 1)^2 <= 2^31 - 1.  Level g = s+1 has s pairs.  Prefer splitting the
     // pairs of a level over T = 2 TMEM regions (sub-groups of G pairs) over draining K chunks.

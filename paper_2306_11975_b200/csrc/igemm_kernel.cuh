@@ -411,7 +411,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int i = 0; i < S; ++i) {
                         const int p = slice_p(S, i);
-                        // tile parity: tpar flips every tile (S is folded in by the counter)
+                        // tile parity: tpar flips every tile (S is folded in by the counter).
+                        // a_stages is even, so ring slot `as` always holds tiles of the same
+                        // parity: each slot has ONE consumer warp, which waits on every phase
+                        // of it in order (with an odd ring a warp would skip the other warp's
+                        // phases of a slot and a parity wait could then pass on a phase that
+                        // has not completed).
                         if (((tpar + (uint32_t)i) & 1u) == me) {
                             long long c2 = P.stats ? clock64() : 0;
                             ptx::mbar_wait(&a_full[as], aph);
