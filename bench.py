@@ -60,6 +60,26 @@ def env_int(name, default):
         return default
 
 
+def library_int8_context():
+    """cuBLASLt INT8 / FP8 throughput measured on this pool's B200s by tools/int8_peak.py
+    (16384^3, random operands; committed log), the library rate our INT8 work compares to."""
+    p = os.path.join(ROOT, "profiles", "r01b", "cublaslt_int8_fp8_16384.log")
+    out = {"source": "profiles/r01b/cublaslt_int8_fp8_16384.log (tools/int8_peak.py)"}
+    try:
+        for line in open(p):
+            d = json.loads(line)
+            if "error" in d:
+                continue
+            key = "cublaslt_int8" if "int8" in d["op"] and "random" in d["op"] else (
+                "cublaslt_fp8" if "fp8" in d["op"] else None)
+            if key:
+                out[key + "_burst_tops"] = round(d["burst_tops"], 1)
+                out[key + "_sustained_tops"] = round(d["sustained_tops"], 1)
+    except (OSError, ValueError, KeyError):
+        return None
+    return out
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -452,7 +472,8 @@ def main():
                 "ops_per_launch": int8_ops_launch, "ops": "INT8 ops (2 per MAC) = s(s+1) m_loc n k",
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json; {INT8_PEAK_NOTE}",
                 "gemm_ms": gemm_ms, "slice_ms": slice_ms,
-                "gemm_share_of_step": (gemm_ms / ms) if gemm_ms else None}
+                "gemm_share_of_step": (gemm_ms / ms) if gemm_ms else None,
+                "library_context": library_int8_context()}
 
     # ---- cuBLAS DGEMM on the same GPUs (row block, B resident: no communication) -----
     cublas = None
