@@ -175,6 +175,25 @@ def cpu_baseline_sample(A, B, k, s, target_s=15.0):
     return value, dt, desc, (rows, cols, Cs)
 
 
+def cpu_phase_breakdown(A, B, k, s, rows, cols):
+    """The oracle's phases on the same sample, timed separately (the paper's Fig. 9 split,
+    P:613-620): slicing of the sampled rows of A and columns of B, the s(s+1)/2 INT32 pair
+    products, and the whole call minus those (accumulation + scaling)."""
+    import oracle as O
+    As, Bs = np.asfortranarray(A[rows]), np.asfortranarray(B[:, cols])
+    rn, cn = len(rows), len(cols)
+    t = time.perf_counter()
+    da, _, _ = O.split_opA(As, "N", rn, k, rn, s)
+    db, _, _ = O.split_opB(Bs, "N", k, cn, k, s)
+    t_split = time.perf_counter() - t
+    t = time.perf_counter()
+    for p in range(1, s + 1):
+        for q in range(1, s + 2 - p):
+            O.int_gemm(da[p - 1], db[q - 1])
+    t_pairs = time.perf_counter() - t
+    return {"split_s": t_split, "pair_products_s": t_pairs}
+
+
 def run_reference(args, wl):
     """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
     rank = env_int("RANK", 0)
@@ -574,6 +593,11 @@ def main():
         cv_, dt_, desc, (rows, cols, Cs) = cpu_baseline_sample(A, B, k, s)
         cpu = {"value": cv_, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
                "sample": desc, "seconds": dt_}
+        ph = cpu_phase_breakdown(A, B, k, s, rows, cols)
+        ph["accumulate_s"] = max(0.0, dt_ - ph["split_s"] - ph["pair_products_s"])
+        ph["note"] = ("oracle phases on the same sample (P:613-620 Fig. 9 split): accumulate = "
+                      "whole call - split - pair products")
+        cpu["phases"] = ph
         Cg = dC.view(n, m).t()[torch.as_tensor(rows, device=dev)][:, torch.as_tensor(cols, device=dev)]
         Cg = Cg.cpu().numpy()
         import oracle as O
