@@ -85,8 +85,6 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     }
     p->tile_n = nc;
     p->k_block = kKB;
-    static const char *pf_env = getenv("OZIMMU_PREFETCH_KB");  // experiments
-    p->prefetch_kb = pf_env ? atoi(pf_env) : 0;  // measured: L2 prefetch slows the B ring
     p->a_stages = a_stages;
     p->b_stages = b_stages;
     p->stages = a_stages;

@@ -43,7 +43,6 @@ struct KParams {
     unsigned int *wave_counter;  // soft grid barrier between tile waves (may be null)
     int64_t full_waves;          // waves in which every CTA has a tile
     long long *stats;            // optional per-CTA stall counters (kStatSlots per CTA) or null
-    int prefetch_kb;             // L2 prefetch distance in k-blocks (0 = off)
     int G;                       // pairs per INT32 accumulator (sub-group size)
     int T;                       // accumulator regions (sub-groups) per level, 1 or 2
     uint32_t region_col[2];      // TMEM column of region t (region t holds levels j < s - tG)
@@ -196,7 +195,7 @@ __device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[
 template <int S>
 __global__ void __launch_bounds__(kThreads, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmApf, const KParams P) {
+              const KParams P) {
     constexpr int NC = nc_for(S);
     __shared__ int32_t eb_s[2][64];  // column exponents of the current tile (double-buffered)
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
@@ -242,7 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 4 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
-        ptx::tma_prefetch_desc(&tmApf);
     }
     if (warp == 0) {
         ptx::tmem_alloc(tmem_slot, P.tmem_cols);
@@ -263,14 +261,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t wave = 0;
             long long st_w = 0, st_pa = 0, st_pb = 0;
             const uint32_t b_tx = (uint32_t)(s * NC * kKB), a_tx = (uint32_t)(kBlockM * kKB);
-            constexpr int kPfS = S < 8 ? S : 8;  // slices per L2-prefetch box
-            auto prefetch = [&](int64_t kb, int64_t mb, int64_t nb) {
-                const int32_t kc = (int32_t)(kb * kKB);
-                ptx::tma_prefetch_l2_3d(&tmB, kc, (int32_t)(nb * NC), 0);
-#pragma unroll
-                for (int z = 0; z < S; z += kPfS)
-                    ptx::tma_prefetch_l2_3d(&tmApf, kc, (int32_t)(mb * kBlockM), z);
-            };
             for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl, ++wave) {
                 int64_t mb, nb;
                 tile_coords(u, P, rank, mb, nb);
@@ -282,11 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // sums are order-independent; K chunks (int64 partials) keep the forward order.
                 const bool rev = OZ_KSNAKE && P.k_chunks == 1 && (wave & 1);
                 auto kmap = [&](int64_t kb) { return rev ? P.num_k_blocks - 1 - kb : kb; };
-                for (int64_t kb = 0; kb < P.prefetch_kb && kb < P.num_k_blocks; ++kb)
-                    prefetch(kmap(kb), mb, nb);
                 for (int64_t kb = 0; kb < P.num_k_blocks; ++kb) {
-                    if (P.prefetch_kb && kb + P.prefetch_kb < P.num_k_blocks)
-                        prefetch(kmap(kb + P.prefetch_kb), mb, nb);
                     const int64_t kx = kmap(kb);
                     long long c1 = P.stats ? clock64() : 0;
                     ptx::mbar_wait(&b_empty[bs], bph ^ 1);
@@ -757,10 +743,6 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     if (!make_map(&tmB, a.b_planes, a.k_pad, a.n, a.s, (uint32_t)(NC / clm),
                   clm == 1 ? (uint32_t)a.s : 1u, a.b_plane_rows))
         return cudaErrorInvalidValue;
-    CUtensorMap tmApf;  // up to 8 A-slice tiles of a k-block per box (L2 prefetch only)
-    if (!make_map(&tmApf, a.a_planes, a.k_pad, a.m, a.s, kBlockM, (uint32_t)(a.s < 8 ? a.s : 8),
-                  a.a_plane_rows))
-        return cudaErrorInvalidValue;
     KParams P;
     P.m = a.m;
     P.n = a.n;
@@ -793,7 +775,6 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.scratch = p.k_chunks > 1 ? a.chunk_scratch : nullptr;
     P.wave_counter = a.wave_counter;
     P.stats = a.stats;
-    P.prefetch_kb = p.prefetch_kb;
     P.G = p.G;
     P.T = p.T;
     P.region_col[0] = 0;
@@ -810,7 +791,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
         if (e != cudaSuccess) return e;
     }
     if (cl == 1) {
-        kern<<<grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, tmApf, P);
+        kern<<<grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, P);
         return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
@@ -824,7 +805,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmApf, P);
+    return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, P);
 }
 
 }  // namespace gemm_detail

@@ -92,7 +92,6 @@ struct GemmPlan {
     int64_t chunk_blocks;  // k-blocks per INT32-safe chunk
     int k_chunks;
     int G, T;          // INT32 sub-groups: T regions of <= G pairs per level
-    int prefetch_kb;   // TMA L2 prefetch distance (k-blocks)
     int grid;
     size_t smem_bytes;
     int tmem_cols;

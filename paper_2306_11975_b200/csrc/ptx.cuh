@@ -70,14 +70,6 @@ __device__ __forceinline__ void tma_load_3d(const void *desc, uint64_t *bar, voi
         "l"(cache_hint)
         : "memory");
 }
-// 3-D tiled prefetch global -> L2 (no shared-memory destination).
-__device__ __forceinline__ void tma_prefetch_l2_3d(const void *desc, int32_t c0, int32_t c1,
-                                                   int32_t c2) {
-    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
-                     reinterpret_cast<uint64_t>(desc)),
-                 "r"(c0), "r"(c1), "r"(c2)
-                 : "memory");
-}
 // L2 cache-policy constants (createpolicy.fractional.L2::evict_{first,last} with fraction 1.0)
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
