@@ -351,6 +351,9 @@ def main():
                     help="fixed s; 0 = INT8-AUTO with --auto-T (P:656-659)")
     ap.add_argument("--auto-T", type=float, default=0.0)
     ap.add_argument("--chunk-cols", type=int, default=2048)
+    ap.add_argument("--grid", default=None,
+                    help="PRxPC: 2-D partition of C over the N ranks (SURVEY s8e 'large n'); "
+                         "default: row blocks")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
@@ -395,8 +398,15 @@ def main():
     dev = torch.device("cuda", local)
     m, n, k, s = wl["m"], wl["n"], wl["k"], wl["s"]
     s_call = s  # 0 = INT8-AUTO: every step runs the mantissa-loss scan
-    r0, r1 = D.row_range(m, world, rank)
-    ml = r1 - r0
+    pr, pc = world, 1
+    if args.grid and world > 1:
+        pr, pc = (int(x) for x in args.grid.lower().split("x"))
+        assert pr * pc == world, f"--grid {args.grid} needs {pr * pc} ranks, got {world}"
+    gi, gj = D.grid_coords(rank, pr, pc)
+    r0, r1 = D.row_range(m, pr, gi)
+    n0, n1 = D.row_range(n, pc, gj)
+    ml, nl = r1 - r0, n1 - n0
+    groups = D.make_grid_groups(pr, pc, 0) if pc > 1 else None
 
     # ---- inputs (identical bytes to the oracle's: synth.gen_phi) ------------------
     A = synth.gen_phi(m, k, wl["phi"], wl["seeds"][0])
@@ -405,7 +415,7 @@ def main():
     B_h = torch.from_numpy(B.ravel(order="F")) if B is not None else None
     dA = A_loc_h.to(dev)
     dB = B_h.to(dev) if B_h is not None else None
-    dC = torch.empty(ml * n, dtype=torch.float64, device=dev)
+    dC = torch.empty(ml * nl, dtype=torch.float64, device=dev)
     lda = max(1, ml)
 
     h = oz.Handle(local)
@@ -420,6 +430,10 @@ def main():
         nonlocal bufs
         if world == 1:
             h.dgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, s_call)
+        elif groups is not None:
+            bufs = D.dgemm_grid2d(be, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0, dC, lda,
+                                  s_call, pr, pc, groups, root=0, chunk_cols=args.chunk_cols,
+                                  bufs=bufs)
         else:
             bufs = D.dgemm_rowblock(be, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0,
                                     dC.view(n, ml).t() if ml else dC, lda, s_call, root=0,
@@ -466,7 +480,9 @@ def main():
     slice_ms = float(np.mean([p["slice_a_ms"] + p["slice_b_ms"] for p in phases])) if phases else None
     peaks, peak_src = load_peaks()
     int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    int8_ops_launch = float(s * (s + 1)) * ml * n * k  # 2 ops per INT8 MAC, s(s+1)/2 pairs
+    # one library GEMM call = the whole product at N = 1, one B column chunk at N > 1
+    n_launch = n if world == 1 else min(args.chunk_cols, nl)
+    int8_ops_launch = float(s * (s + 1)) * ml * n_launch * k  # 2 ops per INT8 MAC
     achieved = int8_ops_launch / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")
@@ -488,7 +504,9 @@ def main():
                 "frac_of_burst_peak": (achieved / int8_burst) if achieved else None,
                 "tensor_util_at_measured_clock": (achieved / hw_at_clock)
                 if (achieved and hw_at_clock) else None,
-                "ops_per_launch": int8_ops_launch, "ops": "INT8 ops (2 per MAC) = s(s+1) m_loc n k",
+                "ops_per_launch": int8_ops_launch,
+                "ops": "INT8 ops (2 per MAC) = s(s+1) m_loc n_launch k (n_launch = n at N = 1, "
+                       "one B chunk at N > 1)",
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json; {INT8_PEAK_NOTE}",
                 "gemm_ms": gemm_ms, "slice_ms": slice_ms,
                 "gemm_share_of_step": (gemm_ms / ms) if gemm_ms else None,
@@ -501,8 +519,8 @@ def main():
         if world > 1:
             dist.broadcast(Bt, src=0)
         Am = dA.view(k, ml).t() if ml else None
-        Bm = Bt.view(n, k).t()
-        Cm = torch.empty(ml, n, dtype=torch.float64, device=dev)
+        Bm = Bt.view(n, k).t()[:, n0:n1]
+        Cm = torch.empty(ml, nl, dtype=torch.float64, device=dev)
 
         def cstep():
             if ml:
@@ -524,7 +542,7 @@ def main():
         cv = flops / (cms / 1e3) / 1e12
         cublas = {"value": cv, "unit": "TFLOP/s", "ms_per_step": cms,
                   "frac_of_fp64_peak_40": cv / 40.0 / world, "speedup_ozimmu_vs_cublas": value / cv,
-                  "note": "torch.matmul float64 (cuBLAS DGEMM), same row blocks, B already resident"}
+                  "note": "torch.matmul float64 (cuBLAS DGEMM), same C blocks, B already resident"}
         del Cm
         if world > 1:
             del Bt
@@ -534,7 +552,7 @@ def main():
     if not args.no_e2e:
         A_pin = A_loc_h.pin_memory()
         B_pin = B_h.pin_memory() if B_h is not None else None
-        C_pin = torch.empty(ml * n, dtype=torch.float64).pin_memory()
+        C_pin = torch.empty(ml * nl, dtype=torch.float64).pin_memory()
         h2d = A_pin.numel() * 8 + (B_pin.numel() * 8 if B_pin is not None else 0)
         d2h = C_pin.numel() * 8
 
@@ -611,8 +629,11 @@ def main():
 
     launches_per_step = rep.get("launches", 0)
     if world > 1:
-        nch = len(D.col_chunks(n, args.chunk_cols))
-        launches_per_step = nch * (rep.get("launches", 0)) + (nch * 1 if rank == 0 else 0)
+        # rank 0's count: it slices every B chunk (one launch each) and runs its own chunks
+        nch = len(D.col_chunks(nl, args.chunk_cols))
+        nall = sum(len(D.col_chunks(b - a, args.chunk_cols))
+                   for a, b in (D.row_range(n, pc, jj) for jj in range(pc)))
+        launches_per_step = nch * (rep.get("launches", 0)) + (nall if rank == 0 else 0)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -620,8 +641,10 @@ def main():
         "dtype": "i8", "data": "synthetic",
         "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "phi": wl["phi"],
                    "seeds": list(wl["seeds"]), "auto": wl.get("auto"),
-                   "parallelism": "single GPU" if world == 1 else
-                   f"C row blocks x{world} + chunked NCCL broadcast of B slices",
+                   "parallelism": "single GPU" if world == 1 else (
+                       f"C row blocks x{world} + chunked NCCL broadcast of B slices" if pc == 1
+                       else f"C {pr}x{pc} blocks + chunked NCCL broadcast of each column "
+                            f"block's B slices within its grid column"),
                    "l2": "inputs larger than L2 (each operand 2.1 GB fp64 + 2.4 GB int8 planes)",
                    "io_dtype": "f64 in/out; i8 x i8 -> i32 tensor-core products; f64 epilogue",
                    "plan": {kk: rep[kk] for kk in ("tile_n", "k_block", "stages", "k_chunks",

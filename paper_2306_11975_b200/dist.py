@@ -104,3 +104,71 @@ def dgemm_rowblock(backend, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, l
     if overlap is not None and world > 1:
         overlap(False)
     return bufs
+
+
+def grid_coords(rank, pr, pc):
+    """Rank -> (i, j) on a pr x pc process grid (row-major): C block row i, column block j."""
+    return divmod(rank, pc)
+
+
+def make_grid_groups(pr, pc, root=0):
+    """Process groups for dgemm_grid2d: G_j = {root} + the ranks of grid column j.
+    Collective: every rank must call it (torch.distributed.new_group), in the same order."""
+    groups = []
+    for j in range(pc):
+        members = sorted({root} | {i * pc + j for i in range(pr)})
+        groups.append((members, dist.new_group(ranks=members)))
+    return groups
+
+
+def dgemm_grid2d(backend, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta, C_loc,
+                 ldc, s, pr, pc, groups, root=0, chunk_cols=2048, bufs=None):
+    """2-D partition of C ('large n'): rank (i, j) of a pr x pc grid owns rows
+    row_range(m, pr, i) and columns row_range(n, pc, j) of C.  It slices its own rows of op(A)
+    (A row block i is replicated on the pc ranks of grid row i and sliced there, as the survey
+    proposes, so there is still no collective but the B one), and receives only the B-slice
+    buffers of its column block: the root slices op(B) chunk by chunk and broadcasts chunk c
+    of column block j inside group G_j = {root} + column j (make_grid_groups).  Every C element
+    is still computed on one GPU by the canonical operation sequence: C is bitwise equal to
+    the single-GPU result.  C_loc: this rank's m_loc x n_loc block (ldc); returns the buffers."""
+    rank = dist.get_rank()
+    i, j = grid_coords(rank, pr, pc)
+    plan = []  # (column block jj, c0, c1) in the order the root slices / broadcasts them
+    for jj in range(pc):
+        n0, n1 = row_range(n, pc, jj)
+        for c0, c1 in col_chunks(n1 - n0, chunk_cols):
+            plan.append((jj, n0 + c0, n0 + c1))
+    mine = [(jj, c0, c1) for jj, c0, c1 in plan if jj == j]
+    if bufs is None:
+        bufs = {}
+    works = {}
+    for jj, c0, c1 in plan:
+        members, grp = groups[jj]
+        if rank not in members:
+            continue
+        key = (c0, c1)
+        if key not in bufs:
+            bufs[key] = backend.alloc(backend.b_slices_bytes(c1 - c0, k, s))
+        buf = bufs[key]
+        if rank == root:
+            backend.slice_b(transB, k, c0, c1, B, ldb, s, buf)
+        works[key] = dist.broadcast(buf, src=root, group=grp, async_op=True) \
+            if len(members) > 1 else None
+    n0, _ = row_range(n, pc, j)
+    overlap = getattr(backend, "overlap", None)
+    for q, (jj, c0, c1) in enumerate(mine):
+        w = works.get((c0, c1))
+        if w is not None:
+            w.wait()
+        if overlap is not None:
+            overlap(q < len(mine) - 1)
+        if m_loc > 0:
+            backend.gemm(transA, m_loc, c0 - n0, c1 - n0, k, alpha, A_loc, lda, bufs[(c0, c1)],
+                         beta, C_loc, ldc, s)
+    if overlap is not None:
+        overlap(False)
+    # the root may also have broadcast other columns' chunks: complete them before returning
+    for key, w in works.items():
+        if w is not None and not any((c0, c1) == key for _, c0, c1 in mine):
+            w.wait()
+    return bufs

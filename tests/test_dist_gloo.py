@@ -107,3 +107,56 @@ def test_row_range_and_chunks():
             assert max(r1 - r0 for r0, r1 in rr) - min(r1 - r0 for r0, r1 in rr) <= 1
     assert D.col_chunks(10, 4) == [(0, 4), (4, 8), (8, 10)]
     assert D.col_chunks(0, 4) == []
+
+
+def _worker2d(rank, world, port, cfg, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, n, k, s, ta, tb, root, chunk, pr, pc = cfg
+        groups = D.make_grid_groups(pr, pc, root)
+        A = synth.gen_phi(*(m, k) if ta == "N" else (k, m), 1.0, 15)
+        B = synth.gen_phi(*(k, n) if tb == "N" else (n, k), 1.0, 16)
+        Cin = synth.gen_phi(m, n, 0.5, 17)
+        i, j = D.grid_coords(rank, pr, pc)
+        r0, r1 = D.row_range(m, pr, i)
+        n0, n1 = D.row_range(n, pc, j)
+        A_loc = np.asfortranarray(A[r0:r1] if ta == "N" else A[:, r0:r1])
+        lda = A_loc.shape[0] if A_loc.shape[0] > 0 else 1
+        C_loc = np.asfortranarray(Cin[r0:r1, n0:n1]).copy()
+        D.dgemm_grid2d(OracleBackend(), ta, tb, r1 - r0, n, k, 1.5, A_loc, lda,
+                       B if rank == root else None, B.shape[0], -0.5, C_loc, max(1, r1 - r0), s,
+                       pr, pc, groups, root=root, chunk_cols=chunk)
+        q.put((rank, r0, r1, n0, n1, C_loc))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [
+    (37, 50, 40, 9, "N", "N", 0, 16, 2, 2),
+    (20, 64, 33, 7, "T", "N", 3, 8, 2, 2),   # root in grid column 1
+    (9, 30, 21, 11, "N", "T", 0, 7, 1, 3),   # column blocks only
+    (30, 9, 21, 5, "N", "N", 1, 4, 3, 1),    # row blocks only
+])
+def test_grid2d_broadcast_matches_single_process(cfg):
+    m, n, k, s, ta, tb, root, chunk, pr, pc = cfg
+    world = pr * pc
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker2d, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    A = synth.gen_phi(*(m, k) if ta == "N" else (k, m), 1.0, 15)
+    B = synth.gen_phi(*(k, n) if tb == "N" else (n, k), 1.0, 16)
+    Cin = synth.gen_phi(m, n, 0.5, 17)
+    ref = O.dgemm(ta, tb, m, n, k, 1.5, A, A.shape[0], B, B.shape[0], -0.5, Cin, m, s)
+    C = np.full((m, n), np.nan)
+    for rank, r0, r1, n0, n1, Cl in parts:
+        C[r0:r1, n0:n1] = Cl
+    assert np.array_equal(C, ref)

@@ -104,3 +104,59 @@ def test_rowblock_broadcast_cuda_backend_bitwise(cfg):
     assert np.array_equal(C, one)
     ref = O.dgemm(ta, tb, m, n, k, 1.5, A, A.shape[0], B, B.shape[0], -0.5, Cin, m, s)
     assert np.array_equal(C, ref)
+
+
+def _worker2d(rank, world, port, cfg, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import paper_2306_11975_b200 as oz
+    from paper_2306_11975_b200 import dist as D
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        m, n, k, s, ta, tb, root, chunk, pr, pc = cfg
+        groups = D.make_grid_groups(pr, pc, root)
+        A, B, Cin = _inputs(cfg[:8])
+        i, j = D.grid_coords(rank, pr, pc)
+        r0, r1 = D.row_range(m, pr, i)
+        n0, n1 = D.row_range(n, pc, j)
+        ml = r1 - r0
+        A_loc = np.asfortranarray(A[r0:r1] if ta == "N" else A[:, r0:r1])
+        dA = torch.from_numpy(A_loc.ravel(order="F").copy()).to(dev)
+        dB = torch.from_numpy(B.ravel(order="F").copy()).to(dev) if rank == root else None
+        dC = torch.from_numpy(np.asfortranarray(Cin[r0:r1, n0:n1]).ravel(order="F").copy()).to(dev)
+        h = oz.Handle(0)
+        h.set_stream(torch.cuda.current_stream(dev))
+        be = D.CudaBackend(h, dev, reserve_sms=16)
+        D.dgemm_grid2d(be, ta, tb, ml, n, k, 1.5, dA, max(1, A_loc.shape[0]), dB, B.shape[0],
+                       -0.5, dC, max(1, ml), s, pr, pc, groups, root=root, chunk_cols=chunk)
+        torch.cuda.synchronize()
+        q.put((rank, r0, r1, n0, n1, dC.cpu().numpy().reshape(n1 - n0, ml).T.copy()))
+        h.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg", [(300, 260, 130, 9, "N", "N", 0, 64, 2, 2),
+                                 (200, 150, 500, 13, "T", "T", 3, 48, 2, 2)])
+def test_grid2d_cuda_backend_bitwise(cfg):
+    import oracle as O
+    m, n, k, s, ta, tb, root, chunk, pr, pc = cfg
+    world = pr * pc
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker2d, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    A, B, Cin = _inputs(cfg[:8])
+    C = np.full((m, n), np.nan)
+    for rank, r0, r1, n0, n1, Cl in parts:
+        C[r0:r1, n0:n1] = Cl
+    ref = O.dgemm(ta, tb, m, n, k, 1.5, A, A.shape[0], B, B.shape[0], -0.5, Cin, m, s)
+    assert np.array_equal(C, ref)
