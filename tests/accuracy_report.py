@@ -1,7 +1,8 @@
 """Accuracy evidence on the GPU (test infrastructure; run on a B200, writes JSON):
   * BASELINE config 2: 1024^3, phi in {0.1, 0.5, 1, 2, 4}, s = 3..13 -- mean / normwise-max /
     literal-max relative error vs double-double (64 sampled rows x all columns) for the
-    tcgen05 path and cuBLAS DGEMM, and the FP64-equivalent s per phi (SURVEY s8c gate);
+    tcgen05 path (canonical mode L), the oracle's paper-literal Alg. 3 order (mode P) and
+    cuBLAS DGEMM, and the FP64-equivalent s per phi (SURVEY s8c gate);
     reproduces the paper's Fig. 6 trends.
   * NEXT row f4: A * A_dag zero-cancellation workload, n = 1024.
 usage: python tests/accuracy_report.py out.json"""
@@ -45,6 +46,10 @@ def main(out):
         for s in range(3, 14):
             st = O.err_stats(ozaki(h, A, B, s)[rows], hi, lo)
             row[f"s{s}"] = st
+            # the paper-literal Alg. 3 accumulation order (oracle mode P, reading A6) alongside
+            Cp = O.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, np.zeros((m, n), order="F"), m,
+                         s, mode="P", rows=rows)
+            row[f"s{s}_modeP"] = O.err_stats(Cp[rows], hi, lo)
             if s_eq is None and st["nw_max"] <= 1e-14 and \
                     st["mean_rel"] <= min(1e-14, row["cublas_dgemm"]["mean_rel"]):
                 s_eq = s
