@@ -35,6 +35,8 @@ struct ozimmu_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     void *host_buf = nullptr;
     size_t host_buf_bytes = 0;
+    void *auto_bbuf = nullptr;  // B-slice buffer of the INT8-AUTO host path (grown, kept)
+    size_t auto_bbuf_bytes = 0;
 };
 
 namespace {
@@ -473,6 +475,7 @@ ozimmu_status_t ozimmu_auto_splits(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu
 ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
     if (!h) return OZIMMU_SUCCESS;
     if (h->auto_dev) cudaFree(h->auto_dev);
+    if (h->auto_bbuf) cudaFree(h->auto_bbuf);
     if (h->events) {
         cudaStreamSynchronize(h->stream);
         for (int i = 0; i < 4 * h->timing_cap; ++i) cudaEventDestroy(h->events[i]);
@@ -1118,6 +1121,145 @@ ozimmu_status_t host_full(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t tra
     return cuda_status(e);
 }
 
+// INT8-AUTO with host buffers, pipelined (f2): op(A) row blocks and op(B) column
+// chunks go H2D on one stream while the mantissa-loss scan of each arrived block runs on the
+// compute stream (row / column exponents are local to a block, and the per-s loss sums are
+// additive); one D2H read picks s; B is sliced once, then C is computed in row blocks whose
+// D2H overlaps the next block's GEMM.  Bitwise equal to ozimmu_dgemm with num_slices = 0.
+ozimmu_status_t host_auto(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
+                          int64_t n, int64_t k, const double *alpha, const double *A, int64_t lda,
+                          const double *B, int64_t ldb, const double *beta, double *C,
+                          int64_t ldc) {
+    constexpr int NS = 33;
+    const int s_max = h->auto_smax;
+    const int w = slice_width(k);
+    const bool a_contig = transA != OZIMMU_OP_N, b_contig = transB == OZIMMU_OP_N;
+    const int64_t ar = a_contig ? k : m, ac = a_contig ? m : k;  // stored shapes
+    const int64_t br = b_contig ? k : n, bc = b_contig ? n : k;
+    const size_t sa = align_up(sizeof(double) * (size_t)ar * ac);
+    const size_t sb = align_up(sizeof(double) * (size_t)br * bc);
+    const size_t sc = align_up(sizeof(double) * (size_t)m * n);
+    const size_t sk = align_up(sizeof(int32_t) * (size_t)(m > n ? m : n));
+    ozimmu_status_t st = host_buffers(h, sa + sb + sc + sk);
+    if (st) return st;
+    if (!h->auto_dev && cudaMalloc(&h->auto_dev, 2 * NS * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return OZIMMU_ERR_WORKSPACE;
+    }
+    uint8_t *base = static_cast<uint8_t *>(h->host_buf);
+    double *dA = reinterpret_cast<double *>(base), *dB = reinterpret_cast<double *>(base + sa);
+    double *dC = reinterpret_cast<double *>(base + sa + sb);
+    int32_t *keys = reinterpret_cast<int32_t *>(base + sa + sb + sc);
+    const int64_t nblk = 8;
+    const int64_t mb = round_up(ceil_div(m, nblk), 128), nbk = round_up(ceil_div(n, nblk), 96);
+    const int64_t P = ceil_div(m, mb), J = ceil_div(n, nbk);
+    std::vector<cudaEvent_t> ev((size_t)(P + J + P + 1));
+    cudaError_t e = cudaSuccess;
+    size_t made = 0;
+    for (; made < ev.size() && e == cudaSuccess; ++made)
+        e = cudaEventCreateWithFlags(&ev[made], cudaEventDisableTiming);
+    cudaEvent_t *ev_in = ev.data(), *ev_cdone = ev.data() + P + J, ev_start = ev[ev.size() - 1];
+    cudaStream_t cs = h->stream;
+    int launches = 0;
+    void *bbuf = nullptr;
+    int s = s_max;
+#define OZ_TRY(x) do { if (e == cudaSuccess) e = (x); } while (0)
+    OZ_TRY(cudaEventRecord(ev_start, cs));
+    OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_start, 0));
+    OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_start, 0));
+    OZ_TRY(cudaMemsetAsync(h->auto_dev, 0, 2 * NS * sizeof(unsigned long long), cs));
+    // ---- H2D in blocks, scan each block as it lands ----
+    for (int64_t i = 0; i < P; ++i) {
+        const int64_t r0 = i * mb, mi = (i == P - 1) ? m - r0 : mb;
+        const double *src = a_contig ? dA + r0 * k : dA + r0;
+        if (a_contig)  // stored k x m: op(A) rows r0.. = columns r0..
+            OZ_TRY(copy2d(dA + r0 * k, k, A + r0 * lda, lda, k, mi, cudaMemcpyHostToDevice, h->h2d));
+        else
+            OZ_TRY(copy2d(dA + r0, m, A + r0, lda, mi, k, cudaMemcpyHostToDevice, h->h2d));
+        OZ_TRY(cudaEventRecord(ev_in[i], h->h2d));
+        OZ_TRY(cudaStreamWaitEvent(cs, ev_in[i], 0));
+        OZ_TRY(launch_mantissa_loss(src, a_contig ? k : m, a_contig, mi, k, w, s_max, h->auto_dev,
+                                    keys, h->num_sms, cs, &launches));
+    }
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t c0 = j * nbk, nc = (j == J - 1) ? n - c0 : nbk;
+        const double *src = b_contig ? dB + c0 * k : dB + c0;
+        if (b_contig)  // stored k x n: op(B) columns c0..
+            OZ_TRY(copy2d(dB + c0 * k, k, B + c0 * ldb, ldb, k, nc, cudaMemcpyHostToDevice, h->h2d));
+        else
+            OZ_TRY(copy2d(dB + c0, n, B + c0, ldb, nc, k, cudaMemcpyHostToDevice, h->h2d));
+        OZ_TRY(cudaEventRecord(ev_in[P + j], h->h2d));
+        OZ_TRY(cudaStreamWaitEvent(cs, ev_in[P + j], 0));
+        OZ_TRY(launch_mantissa_loss(src, b_contig ? k : n, b_contig, nc, k, w, s_max,
+                                    h->auto_dev + NS, keys, h->num_sms, cs, &launches));
+    }
+    if (*beta != 0.0) OZ_TRY(copy2d(dC, m, C, ldc, m, n, cudaMemcpyHostToDevice, h->h2d));
+    // ---- choose s (one D2H read) ----
+    unsigned long long sums[2 * NS];
+    OZ_TRY(cudaMemcpyAsync(sums, h->auto_dev, sizeof(sums), cudaMemcpyDeviceToHost, cs));
+    OZ_TRY(cudaStreamSynchronize(cs));
+    OZ_TRY(cudaStreamSynchronize(h->h2d));  // C (beta != 0) is on the device too
+    if (e == cudaSuccess) {
+        for (int q = 1; q <= s_max; ++q) {
+            const double ma = sums[32] ? (double)sums[q - 1] / (double)sums[32] : 0.0;
+            const double mbv = sums[NS + 32] ? (double)sums[NS + q - 1] / (double)sums[NS + 32] : 0.0;
+            if (ma <= h->auto_T && mbv <= h->auto_T) {
+                s = q;
+                break;
+            }
+        }
+        h->auto_last_s = s;
+        const size_t need = ozimmu_b_slices_bytes(n, k, s);
+        if (need > h->auto_bbuf_bytes) {
+            if (h->auto_bbuf) cudaFree(h->auto_bbuf);
+            h->auto_bbuf = nullptr;
+            h->auto_bbuf_bytes = 0;
+            if (cudaMalloc(&h->auto_bbuf, need) != cudaSuccess) {
+                cudaGetLastError();
+                e = cudaErrorMemoryAllocation;
+            } else {
+                h->auto_bbuf_bytes = need;
+            }
+        }
+        bbuf = h->auto_bbuf;
+    }
+    // ---- slice B once, then C row blocks: GEMM i overlaps the D2H of block i-1 ----
+    ozimmu_status_t st2 = OZIMMU_SUCCESS;
+    int64_t total_launches = launches;
+    if (e == cudaSuccess) {
+        st2 = ozimmu_slice_b(h, transB, k, n, dB, b_contig ? k : n, s, bbuf);
+        total_launches += h->report.launches;
+    }
+    int64_t done = 0;
+    for (int64_t i = 0; i < P && e == cudaSuccess && st2 == OZIMMU_SUCCESS; ++i, ++done) {
+        const int64_t r0 = i * mb, mi = (i == P - 1) ? m - r0 : mb;
+        const double *Ai = a_contig ? dA + r0 * k : dA + r0;
+        st2 = ozimmu_dgemm_presliced_b(h, transA, mi, n, k, alpha, Ai, a_contig ? k : m, bbuf,
+                                       beta, dC + r0, m, s);
+        total_launches += h->report.launches;
+        if (st2) break;
+        OZ_TRY(cudaEventRecord(ev_cdone[i], cs));
+        OZ_TRY(cudaStreamWaitEvent(h->d2h, ev_cdone[i], 0));
+        OZ_TRY(copy2d(C + r0, ldc, dC + r0, m, mi, n, cudaMemcpyDeviceToHost, h->d2h));
+    }
+    OZ_TRY(cudaStreamSynchronize(h->d2h));
+    OZ_TRY(cudaStreamSynchronize(cs));
+#undef OZ_TRY
+    if (e != cudaSuccess || st2) {
+        cudaStreamSynchronize(h->h2d);
+        cudaStreamSynchronize(h->d2h);
+        cudaStreamSynchronize(cs);
+    }
+    for (size_t i = 0; i < made; ++i) cudaEventDestroy(ev[i]);
+    if (st2) return st2;
+    if (e != cudaSuccess) return cuda_status(e);
+    GemmPlan gp;
+    plan_gemm(s, w, mb, n, round_up(k, 16), gemm_sms(h), &gp);
+    fill_report(h, s, w, m, n, k, &gp, (int)total_launches,
+                (int64_t)s * (m + n) * round_up(k, 16) + 4 * (m + n));
+    return OZIMMU_SUCCESS;
+}
+
 }  // namespace
 
 extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t transA,
@@ -1136,6 +1278,8 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
         return OZIMMU_SUCCESS;
     }
     if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    if (num_slices == 0 && *alpha != 0.0 && k > 0 && k <= OZIMMU_MAX_K)
+        return host_auto(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
     if (num_slices == 0 || *alpha == 0.0 || k == 0)
         return host_full(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
                          num_slices);

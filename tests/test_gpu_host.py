@@ -120,3 +120,28 @@ def test_host_auto_and_degenerate(h):
     C = Cin.copy(order="F")
     h.dgemm_host("N", "N", m, n, k, 0.0, None, m, None, k, -2.0, C, m, 9)
     assert np.array_equal(C, -2.0 * Cin)
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "T"), ("N", "C")])
+@pytest.mark.parametrize("T", [0.0, 1.0])
+def test_host_auto_pipelined_blocks(h, ta, tb, T):
+    """INT8-AUTO through the host pipeline: blocks scanned as they land (8 row blocks x 8
+    column chunks), s = the oracle's choice, C bitwise equal to the device-pointer AUTO call."""
+    import torch
+    m, n, k = 1100, 900, 300
+    A = synth.gen_phi(*_stored(ta, m, k), 1.5, 41)
+    B = synth.gen_phi(*_stored(tb, k, n), 1.5, 42)
+    Cin = synth.gen_phi(m, n, 1.0, 43)
+    h.set_auto(T, 20)
+    hC = _pinned(Cin)
+    h.dgemm_host(ta, tb, m, n, k, 0.5, _pinned(A), A.shape[0], _pinned(B), B.shape[0], 2.0,
+                 hC, m, 0)
+    s_host = h.report()["num_slices"]
+    got = np.asfortranarray(hC.numpy().reshape(n, m).T)
+    s_ref = O.auto_splits(ta, tb, m, n, k, A, A.shape[0], B, B.shape[0], T, 20)
+    assert s_host == s_ref
+    dC = dev(Cin)
+    h.dgemm(ta, tb, m, n, k, 0.5, dev(A), A.shape[0], dev(B), B.shape[0], 2.0, dC, m, 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, host(dC, m, n))
+    h.set_auto(0.0, 20)
