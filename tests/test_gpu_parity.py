@@ -413,3 +413,21 @@ def test_rowblock_driver_single_gpu_chunks(h, ta, tb, chunk):
     torch.cuda.synchronize()
     got = dC.t().contiguous().view(-1)
     assert np.array_equal(host(got, m, n), full)
+
+
+@pytest.mark.parametrize("cap", [1, 2, 37, 100])
+def test_dgemm_capped_grid_bitwise(cap):
+    """ozimmu_set_max_sms (persistent grid capped to `cap` SMs, CTA pairs rounded down) gives
+    the same bits as the full grid, and 0 restores it."""
+    import paper_2306_11975_b200 as oz
+    m, n, k, s = 600, 500, 700, 9
+    A, B = synth.gen_phi(m, k, 0.5, 71), synth.gen_phi(k, n, 0.5, 72)
+    Cin = np.zeros((m, n), order="F")
+    h = oz.Handle(0)
+    full = run_dgemm(h, "N", "N", m, n, k, 1.0, A, B, 0.0, Cin, s)
+    h.set_max_sms(cap)
+    capped = run_dgemm(h, "N", "N", m, n, k, 1.0, A, B, 0.0, Cin, s)
+    h.set_max_sms(0)
+    again = run_dgemm(h, "N", "N", m, n, k, 1.0, A, B, 0.0, Cin, s)
+    h.close()
+    assert np.array_equal(full, capped) and np.array_equal(full, again)
