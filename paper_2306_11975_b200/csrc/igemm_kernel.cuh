@@ -42,6 +42,7 @@ struct KParams {
     int64_t *scratch;
     unsigned int *wave_counter;  // soft grid barrier between tile waves (may be null)
     int64_t full_waves;          // waves in which every CTA has a tile
+    int wave_lag;                // waves a CTA may run ahead of the slowest one (0 = lockstep)
     long long *stats;            // optional per-CTA stall counters (kStatSlots per CTA) or null
     int G;                       // pairs per INT32 accumulator (sub-group size)
     int T;                       // accumulator regions (sub-groups) per level, 1 or 2
@@ -118,7 +119,8 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
 __device__ __forceinline__ void wave_sync(const KParams &P, int64_t wave) {
     if (!P.wave_counter || wave >= P.full_waves) return;
     atomicAdd(P.wave_counter, 1u);
-    const unsigned int target = (unsigned int)((wave + 1) * gridDim.x);
+    if (wave < P.wave_lag) return;
+    const unsigned int target = (unsigned int)((wave + 1 - P.wave_lag) * gridDim.x);
     const uint64_t t0 = globaltimer();
     while (ld_acquire(P.wave_counter) < target) {
         if (globaltimer() - t0 > 200000ull) break;  // 200 us cap
@@ -786,6 +788,8 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.units_n = ceil_div(P.tiles_n, cln);
     P.num_units = P.units_m * P.units_n;
     P.full_waves = P.num_units / (grid / cl);
+    static const int lag_env = getenv("OZIMMU_WAVE_LAG") ? atoi(getenv("OZIMMU_WAVE_LAG")) : 0;
+    P.wave_lag = lag_env > 0 ? lag_env : 0;
     if (P.wave_counter) {
         e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
         if (e != cudaSuccess) return e;
