@@ -43,6 +43,7 @@ struct KParams {
     unsigned int *wave_counter;  // soft grid barrier between tile waves (may be null)
     int64_t full_waves;          // waves in which every CTA has a tile
     int wave_lag;                // waves a CTA may run ahead of the slowest one (0 = lockstep)
+    int ksync;                   // extra soft barriers every `ksync` k-blocks (0 = per tile only)
     long long *stats;            // optional per-CTA stall counters (kStatSlots per CTA) or null
     int G;                       // pairs per INT32 accumulator (sub-group size)
     int T;                       // accumulator regions (sub-groups) per level, 1 or 2
@@ -116,11 +117,11 @@ __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p) {
 // Soft barrier: CTAs of the persistent grid start tile-wave `wave` together, so that the
 // CTAs sharing A row-blocks / B column-blocks stream the same K range through L2 at the
 // same time.  Bounded wait: never a deadlock if some CTAs are not co-resident.
-__device__ __forceinline__ void wave_sync(const KParams &P, int64_t wave) {
+__device__ __forceinline__ void wave_sync(const KParams &P, int64_t wave, int64_t bidx) {
     if (!P.wave_counter || wave >= P.full_waves) return;
     atomicAdd(P.wave_counter, 1u);
-    if (wave < P.wave_lag) return;
-    const unsigned int target = (unsigned int)((wave + 1 - P.wave_lag) * gridDim.x);
+    if (bidx < P.wave_lag) return;
+    const unsigned int target = (unsigned int)((bidx + 1 - P.wave_lag) * gridDim.x);
     const uint64_t t0 = globaltimer();
     while (ld_acquire(P.wave_counter) < target) {
         if (globaltimer() - t0 > 200000ull) break;  // 200 us cap
@@ -260,14 +261,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (ptx::elect_one()) {
             int bs = 0, as = 0;
             uint32_t bph = 0, aph = 0;
-            int64_t wave = 0;
+            int64_t wave = 0, bidx = 0;  // tile wave, soft-barrier instance
             long long st_w = 0, st_pa = 0, st_pb = 0;
             const uint32_t b_tx = (uint32_t)(s * NC * kKB), a_tx = (uint32_t)(kBlockM * kKB);
             for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl, ++wave) {
                 int64_t mb, nb;
                 tile_coords(u, P, rank, mb, nb);
                 long long c0 = P.stats ? clock64() : 0;
-                wave_sync(P, wave);
+                wave_sync(P, wave, bidx++);
                 if (P.stats) st_w += clock64() - c0;
                 // K snake: odd waves walk K backwards, so a wave starts on the k-blocks the
                 // previous wave (same A row blocks) touched last, still in L2.  The INT32
@@ -276,6 +277,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 auto kmap = [&](int64_t kb) { return rev ? P.num_k_blocks - 1 - kb : kb; };
                 for (int64_t kb = 0; kb < P.num_k_blocks; ++kb) {
                     const int64_t kx = kmap(kb);
+                    if (P.ksync && kb > 0 && kb % P.ksync == 0) {
+                        long long c3 = P.stats ? clock64() : 0;
+                        wave_sync(P, wave, bidx++);
+                        if (P.stats) st_w += clock64() - c3;
+                    }
                     long long c1 = P.stats ? clock64() : 0;
                     ptx::mbar_wait(&b_empty[bs], bph ^ 1);
                     if (P.stats) st_pb += clock64() - c1;
@@ -790,6 +796,8 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.full_waves = P.num_units / (grid / cl);
     static const int lag_env = getenv("OZIMMU_WAVE_LAG") ? atoi(getenv("OZIMMU_WAVE_LAG")) : 0;
     P.wave_lag = lag_env > 0 ? lag_env : 0;
+    static const int ksync_env = getenv("OZIMMU_KSYNC") ? atoi(getenv("OZIMMU_KSYNC")) : 0;
+    P.ksync = ksync_env > 0 ? ksync_env : 0;
     if (P.wave_counter) {
         e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
         if (e != cudaSuccess) return e;
