@@ -163,6 +163,33 @@ __device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[
     const int64_t roff = c_row_off(P.c_rows, row);
     if (P.mode == EPI_DGEMM) {
         double *crow = P.C + roff;
+        // Fast path (every full tile in practice): all NC columns inside C, no stacked-batch
+        // column map, and every scale 2^(E_A + E_B) a normal double -- then X = acc 2^e is
+        // one exact multiply and the loop has no per-element branches.  Same operations as
+        // the general path below, so the same bits.
+        if ((nb + 1) * NC <= P.n && !P.c_cols.per_item && ea != kExpNonFinite) {
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const long long e = (long long)ea + ebt[i];  // no int overflow on the marker
+                ok &= ebt[i] != kExpNonFinite && e >= -1022 && e <= 1023;
+            }
+            if (ok) {
+                double *cp = crow + (nb * NC) * P.ldc;
+                if (P.beta == 0.0) {
+#pragma unroll
+                    for (int i = 0; i < NC; ++i)
+                        cp[i * P.ldc] = __dmul_rn(P.alpha, __dmul_rn(acc[i], pow2(ea + ebt[i])));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < NC; ++i) {
+                        const double X = __dmul_rn(acc[i], pow2(ea + ebt[i]));
+                        cp[i * P.ldc] = __fma_rn(P.alpha, X, __dmul_rn(P.beta, cp[i * P.ldc]));
+                    }
+                }
+                return;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < NC; ++i) {
             const int64_t col = nb * NC + i;
