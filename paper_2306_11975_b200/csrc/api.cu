@@ -37,6 +37,9 @@ struct ozimmu_ctx {
     size_t host_buf_bytes = 0;
     void *auto_bbuf = nullptr;  // B-slice buffer of the INT8-AUTO host path (grown, kept)
     size_t auto_bbuf_bytes = 0;
+    // second stream for slicing op(B) concurrently with op(A) (fork / join by events)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -51,7 +54,7 @@ inline int gemm_sms(ozimmu_handle_t h) {
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {  // workspace carve-up for one dgemm call
-    size_t a_planes, a_exp, b_buf, keys, sync, scratch, total;
+    size_t a_planes, a_exp, b_buf, keys, keys_b, sync, scratch, total;
 };
 
 // B-slice buffer: planes [s][n][k_pad] (reversed slice order) | int32 exponents [n]
@@ -73,6 +76,8 @@ Layout layout(int64_t m, int64_t n, int64_t k_pad, int s, size_t scratch) {
     off += b_buf_bytes(n, k_pad, s);
     L.keys = off;
     off += align_up(sizeof(int32_t) * (size_t)(m > n ? m : n));
+    L.keys_b = off;  // B's exponent-scan scratch (B is sliced concurrently with A)
+    off += align_up(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     L.sync = off;
     off += kAlign;
     L.scratch = off;
@@ -209,12 +214,31 @@ cudaError_t slice_a(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t k,
 // Slice op(B) into a B-slice buffer: columns of op(B) are contiguous along k iff transB == N.
 cudaError_t slice_b(ozimmu_handle_t h, ozimmu_op_t transB, int64_t k, int64_t n, int64_t k_pad,
                     const double *B, int64_t ldb, int s, int w, uint8_t *bbuf, int32_t *keys,
-                    int *launches, BatchMap vm = BatchMap()) {
+                    int *launches, BatchMap vm = BatchMap(), cudaStream_t st = nullptr) {
     const bool contig = transB == OZIMMU_OP_N;
     int8_t *planes = reinterpret_cast<int8_t *>(bbuf);
     int32_t *E = reinterpret_cast<int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s));
     return launch_split(B, ldb, contig, n, k, k_pad, s, w, /*reverse=*/true, planes,
-                        (int64_t)n * k_pad, E, keys, h->num_sms, h->stream, launches, 0, 0, vm);
+                        (int64_t)n * k_pad, E, keys, h->num_sms, st ? st : h->stream, launches, 0,
+                        0, vm);
+}
+
+// Fork / join helpers: work on h->aux runs concurrently with h->stream between them.
+cudaError_t aux_fork(ozimmu_handle_t h) {
+    if (!h->aux) {
+        cudaError_t e = cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(h->ev_fork, h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->aux, h->ev_fork, 0);
+    return e;
+}
+cudaError_t aux_join(ozimmu_handle_t h) {
+    cudaError_t e = cudaEventRecord(h->ev_join, h->aux);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->ev_join, 0);
+    return e;
 }
 
 // f2 INT8-AUTO (reading A17): exact per-s mantissa-loss sums of the rows of
@@ -341,9 +365,16 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     int launches = 0;
     int64_t slice_bytes = (int64_t)s * m * k_pad + 4 * m;
     mark(h, 0);
-    if (!bbuf_ext) {
+    // op(B) is sliced on the handle's second stream while op(A) is sliced on its stream
+    // (separate exponent-scan scratch); the GEMM waits for both.  Phase marks: 0 -> 2 is
+    // the whole (overlapped) slicing.
+    const bool fork = !bbuf_ext;
+    if (fork) {
         uint8_t *b = base + L.b_buf;
-        cudaError_t e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, b, keys, &launches, bmap);
+        cudaError_t e = aux_fork(h);
+        if (e == cudaSuccess)
+            e = slice_b(h, transB, k, n, k_pad, B, ldb, s, w, b,
+                        reinterpret_cast<int32_t *>(base + L.keys_b), &launches, bmap, h->aux);
         if (e != cudaSuccess) return cuda_status(e);
         bbuf = b;
         slice_bytes += (int64_t)s * n * k_pad + 4 * n;
@@ -351,6 +382,7 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     mark(h, 1);
     cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches,
                             amap);
+    if (e == cudaSuccess && fork) e = aux_join(h);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, 2);
     e = fused_gemm(h, gp, m, n, k_pad, s, w, a_planes, EA, reinterpret_cast<const int8_t *>(bbuf),
@@ -476,6 +508,12 @@ ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
     if (!h) return OZIMMU_SUCCESS;
     if (h->auto_dev) cudaFree(h->auto_dev);
     if (h->auto_bbuf) cudaFree(h->auto_bbuf);
+    if (h->aux) {
+        cudaStreamSynchronize(h->aux);
+        cudaStreamDestroy(h->aux);
+        cudaEventDestroy(h->ev_fork);
+        cudaEventDestroy(h->ev_join);
+    }
     if (h->events) {
         cudaStreamSynchronize(h->stream);
         for (int i = 0; i < 4 * h->timing_cap; ++i) cudaEventDestroy(h->events[i]);
