@@ -222,11 +222,11 @@ __device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[
     }
 }
 
-template <int S>
+template <int S, int NCV = nc_for(S)>
 __global__ void __launch_bounds__(kThreads, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const KParams P) {
-    constexpr int NC = nc_for(S);
+    constexpr int NC = NCV;  // output columns per tile (nc_for(S), or 32 for small problems)
     __shared__ int32_t eb_s[2][64];  // column exponents of the current tile (double-buffered)
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -711,10 +711,10 @@ inline bool make_map(CUtensorMap *map, const int8_t *base, int64_t k_pad, int64_
     return r == CUDA_SUCCESS;
 }
 
-template <int S>
+template <int S, int NCV = nc_for(S)>
 cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st) {
-    constexpr int NC = nc_for(S);
-    auto kern = k_oz_gemm<S>;
+    constexpr int NC = NCV;
+    auto kern = k_oz_gemm<S, NCV>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
     if (e != cudaSuccess) return e;
