@@ -5,6 +5,7 @@ Expected values come from: big-integer brute force (Python ints), numpy's
 int64 matmul (a library routine the oracle does not use), exact rationals
 (fractions.Fraction), the paper's / SPEC's worked examples, and closed-form
 error bounds."""
+import os
 from fractions import Fraction
 
 import numpy as np
@@ -12,6 +13,8 @@ import pytest
 
 import oracle as O
 import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 U = Fraction(1, 2 ** 53)  # unit roundoff of binary64
 
@@ -291,3 +294,24 @@ def test_subblock_equals_full():
     rows, cols = [19, 0, 7], [10, 3]
     sub = O.dgemm_simple(A, B, 9, rows=rows, cols=cols)
     assert np.array_equal(sub[np.ix_(rows, cols)], full[np.ix_(rows, cols)])
+
+
+def test_oracle_deterministic_across_thread_counts():
+    """the oracle parallelises over (i, j) only, so every element's operation
+    sequence -- and the bits of C -- must not depend on OMP_NUM_THREADS."""
+    import hashlib
+    import subprocess
+    import sys
+    code = ("import sys, hashlib, numpy as np; sys.path.insert(0, %r); import oracle as O, synth;"
+            "A = synth.gen_phi(70, 300, 1.0, 81); B = synth.gen_phi(300, 50, 1.0, 82);"
+            "C = synth.gen_phi(70, 50, 1.0, 83);"
+            "R = O.dgemm('N', 'N', 70, 50, 300, 0.5, A, 70, B, 300, -1.5, C, 70, 9);"
+            "print(hashlib.sha1(np.ascontiguousarray(R).tobytes()).hexdigest())") % ROOT
+    out = []
+    for th in ("1", "3", "8"):
+        env = dict(os.environ, OMP_NUM_THREADS=th)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=120)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(r.stdout.strip())
+    assert len(set(out)) == 1, out
