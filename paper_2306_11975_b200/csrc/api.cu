@@ -2,6 +2,7 @@
 // workspace, and the launch sequence  slice(A) -> slice(B) -> fused tcgen05 GEMM+epilogue.
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 #include <cstring>
 #include <cstdio>
@@ -1050,6 +1051,10 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     hp->nb = nb;
     // the first and the last block are half-size: the first GEMM waits for less H2D, the
     // last region's D2H (the drain after the last GEMM) moves less
+    // Past ~45 % of an operand the tensor cores are behind the copies (the computable area
+    // grows as a square), so later blocks are twice as large: fewer, larger C regions and
+    // fewer partial last waves (OZIMMU_HOST_GROW=0 keeps equal blocks).
+    static const bool grow = !(getenv("OZIMMU_HOST_GROW") && atoi(getenv("OZIMMU_HOST_GROW")) == 0);
     auto bounds = [](int64_t total, int64_t blk, int64_t align, std::vector<int64_t> &b) {
         b.assign(1, 0);
         int64_t half = round_up(blk / 2, align);
@@ -1061,7 +1066,9 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
         int64_t x = half;
         b.push_back(x);
         while (total - x > blk + half) {
-            x += blk;
+            const int64_t step = (grow && x >= total * 45 / 100 && total - x > 2 * blk + half)
+                                     ? 2 * blk : blk;
+            x += step;
             b.push_back(x);
         }
         if (total - x > half) b.push_back(total - half);
@@ -1071,6 +1078,10 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     bounds(n, nb, 96, hp->cb);
     hp->P = (int64_t)hp->rb.size() - 1;
     hp->J = (int64_t)hp->cb.size() - 1;
+    for (size_t i = 1; i < hp->rb.size(); ++i) mb = std::max(mb, hp->rb[i] - hp->rb[i - 1]);
+    for (size_t i = 1; i < hp->cb.size(); ++i) nb = std::max(nb, hp->cb[i] - hp->cb[i - 1]);
+    hp->mb = mb;  // largest block: staging-buffer and scratch sizes
+    hp->nb = nb;
     size_t scratch = 0;
     const int64_t shapes[3][2] = {{mb, nb}, {m, nb}, {mb, n}};
     for (auto &sh : shapes) {
