@@ -52,6 +52,13 @@ def lib():
         L.oz_ref_mantissa_loss.restype = i32
         L.oz_ref_auto_splits.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, dbl, i32]
         L.oz_ref_auto_splits.restype = i32
+        L.oz_ref_trunc_residual.argtypes = [i32, i64, i64, vp, i64, i32, i32, vp]
+        L.oz_ref_trunc_residual.restype = i32
+        L.oz_ref_acc_eta.argtypes = [vp, vp, i32]
+        L.oz_ref_acc_eta.restype = dbl
+        L.oz_ref_auto_splits_acc.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, dbl, i32,
+                                             ct.POINTER(i32)]
+        L.oz_ref_auto_splits_acc.restype = i32
         L.dd_two_sum.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
         L.dd_two_prod.argtypes = [dbl, dbl, ct.POINTER(dbl), ct.POINTER(dbl)]
         L.dd_gemm_sub.argtypes = [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, i64,
@@ -217,6 +224,38 @@ def auto_splits(transA, transB, m, n, k, A, lda, B, ldb, T, s_max=32):
     if s < 0:
         raise ValueError("oz_ref_auto_splits failed")
     return s
+
+
+def trunc_residual(M, trans, rows, kdim, ld, w, s_max):
+    """f2 accuracy-targeted AUTO (reading A18): rho[t], t = 0..s_max = max over the vectors
+    of op(M) of the relative l1 truncation residual after t digits (fixed-point, upper
+    estimate).  trans 0: vector r = M[r + l*ld]; 1: M[l + r*ld]."""
+    M = _f64(M)
+    rho = np.zeros(s_max + 1)
+    rc = lib().oz_ref_trunc_residual(int(trans), rows, kdim, _p(M), int(ld), int(w), int(s_max),
+                                     _p(rho))
+    if rc:
+        raise ValueError(f"oz_ref_trunc_residual failed rc={rc}")
+    return rho
+
+
+def acc_eta(rhoA, rhoB, s):
+    """eta(s) = sum_{t=0..s} rhoA[t] rhoB[s-t] (reading A18)."""
+    ra = np.ascontiguousarray(rhoA, dtype=np.float64)
+    rb = np.ascontiguousarray(rhoB, dtype=np.float64)
+    return lib().oz_ref_acc_eta(_p(ra), _p(rb), int(s))
+
+
+def auto_splits_acc(transA, transB, m, n, k, A, lda, B, ldb, tau=1.0, s_max=18):
+    """f2 accuracy-targeted INT8-AUTO (reading A18): (s, capped)."""
+    A = _f64(A)
+    B = _f64(B)
+    capped = ct.c_int(0)
+    s = lib().oz_ref_auto_splits_acc(OP[transA], OP[transB], m, n, k, _p(A), lda, _p(B), ldb,
+                                     float(tau), int(s_max), ct.byref(capped))
+    if s < 0:
+        raise ValueError("oz_ref_auto_splits_acc failed")
+    return s, bool(capped.value)
 
 
 def _c128(a):

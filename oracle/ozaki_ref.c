@@ -502,3 +502,122 @@ int oz_ref_auto_splits(int transA, int transB, int64_t m, int64_t n, int64_t k,
     }
     return s_max;
 }
+
+/* ---- f2 INT8-AUTO, accuracy-targeted selection (reading A18) -----------
+ *
+ * The Discussion says the loss criterion "does not yield the optimal number of
+ * splits", because the DGEMM rounding error grows with the accumulation length while the
+ * Ozaki error does not ("the accumulation length should be one of the key factors").
+ * Reading A18 writes the error of the method (Alg. 3 keeps the pairs p + q <= s + 1)
+ * elementwise: with a^(t) the first t digits of a (Alg. 4), R_a(t) = a - a^(t)
+ * and R_a(0) = a,
+ *     C - C_s = sum_l sum_{q=1..s} b_q-part (a - a^(s+1-q)) + a (b - b^(s)),
+ * |b_q-part| <= |R_b(q-1)|, hence |C - C_s|_ij <= sum_{t=0..s} (|R_A(t)| |R_B(s-t)|)_ij.
+ * With magnitudes independent along l, (|X||Y|)_ij ~ ||x_i||_1 ||y_j||_1 / k, so relative to
+ * (|A||B|)_ij the predicted error is eta(s) = sum_{t=0..s} rho_A(t) rho_B(s-t), where
+ * rho_v(t) = ||R_v(t)||_1 / ||v||_1 for one vector (row of op(A) / column of op(B)) and
+ * rho_A(t) = max over the rows (rho_B: over the columns), rho(0) = 1.  FP64 DGEMM's own
+ * error in the same units is u sqrt(k) (probabilistic form of gamma_k |A||B|, u = 2^-53), so
+ * s = the smallest s <= s_max with eta(s) <= tau u sqrt(k) (tau = 1: "FP64-equivalent").
+ *
+ * Evaluation, exact and order-free so that any implementation takes the same decision: the
+ * l1 sums are taken in 32-bit fixed point relative to 2^E, the residual terms rounded UP and
+ * the norm terms rounded DOWN (so rho is an upper estimate), as integers:
+ *     N_t(v) = sum_x ceil(frac(|x| 2^(wt - E)) 2^32),   D(v) = sum_x floor(|x| 2^(32 - E)),
+ *     rho_v(t) = ((double)N_t / (double)D) 2^(-wt)   (N, D < 2^53: exact conversions).
+ * Vectors holding NaN/Inf or only zeros are skipped; an operand with no other vector has
+ * rho(t) = 0 for all t (its product is exactly zero or NaN).                           */
+
+/* |x| = M 2^(e - 53) with M an integer, 2^52 <= M < 2^53 (normal) or < 2^52 (subnormal) */
+static void sig_exp(double x, uint64_t *M, int *e)
+{
+    double f = frexp(fabs(x), e); /* |x| = f 2^e, f in [0.5, 1) */
+    *M = (uint64_t)ldexp(f, 53);  /* exact: f has at most 53 significant bits */
+}
+
+/* ceil(frac(|x| 2^(wt - E)) 2^32): |x| 2^(wt-E) = M 2^-z with z = 53 + E - e - wt fraction bits */
+static uint64_t resid_up32(double x, int E, int w, int t)
+{
+    uint64_t M;
+    int e;
+    sig_exp(x, &M, &e);
+    int z = 53 + E - e - w * t;
+    if (z <= 0) return 0; /* |x| 2^(wt-E) is an integer: nothing left after t digits */
+    unsigned __int128 R = z >= 64 ? (unsigned __int128)M : (unsigned __int128)(M % ((uint64_t)1 << z));
+    if (z <= 32) return (uint64_t)(R << (32 - z)); /* exact */
+    int d = z - 32;                                 /* ceil(R / 2^d) */
+    if (d >= 64) return R != 0;
+    return (uint64_t)((R + (((unsigned __int128)1 << d) - 1)) >> d);
+}
+
+/* floor(|x| 2^(32 - E)) = floor(M 2^(e - 53 + 32 - E)) */
+static uint64_t norm_dn32(double x, int E)
+{
+    uint64_t M;
+    int e;
+    sig_exp(x, &M, &e);
+    int d = 53 + E - e - 32; /* >= 21 since e <= E */
+    return d >= 64 ? 0 : M >> d;
+}
+
+/* rho[t], t = 0..s_max, of the vectors of op(M): trans = 0 -> vector r = M[r + l ld]
+ * (rows of op(A) with transA = N), trans = 1 -> M[l + r ld]. */
+int oz_ref_trunc_residual(int trans, int64_t rows, int64_t kdim, const double *M, int64_t ld,
+                          int w, int s_max, double *rho)
+{
+    if (rows < 0 || kdim < 0 || s_max < 1 || s_max > 64 || w < 1) return OZR_ERR_ARG;
+    for (int t = 0; t <= s_max; ++t) rho[t] = 0.0;
+    for (int64_t r = 0; r < rows; ++r) {
+        double vmax = 0.0;
+        int bad = 0;
+        for (int64_t l = 0; l < kdim; ++l) {
+            double v = trans == 0 ? M[r + l * ld] : M[l + r * ld];
+            if (!isfinite(v)) bad = 1;
+            else if (fabs(v) > vmax) vmax = fabs(v);
+        }
+        if (bad || vmax == 0.0) continue;
+        int E;
+        (void)frexp(vmax, &E);
+        uint64_t D = 0, N[65];
+        for (int t = 1; t <= s_max; ++t) N[t] = 0;
+        for (int64_t l = 0; l < kdim; ++l) {
+            double v = trans == 0 ? M[r + l * ld] : M[l + r * ld];
+            if (v == 0.0) continue;
+            D += norm_dn32(v, E);
+            for (int t = 1; t <= s_max; ++t) N[t] += resid_up32(v, E, w, t);
+        }
+        rho[0] = 1.0;
+        for (int t = 1; t <= s_max; ++t) {
+            double q = ldexp((double)N[t] / (double)D, -w * t);
+            if (q > rho[t]) rho[t] = q;
+        }
+    }
+    return OZR_OK;
+}
+
+/* eta(s) = sum_{t=0..s} rho_A(t) rho_B(s - t), summed in the order t = 0, 1, .., s. */
+double oz_ref_acc_eta(const double *rhoA, const double *rhoB, int s)
+{
+    double eta = 0.0;
+    for (int t = 0; t <= s; ++t) eta = eta + rhoA[t] * rhoB[s - t];
+    return eta;
+}
+
+/* Smallest s in [1, s_max] with eta(s) <= tau u sqrt(k), u = 2^-53 (reading A18); s_max if
+ * none (then *capped = 1).  k is the accumulation length (2k for the complex embedding A16). */
+int oz_ref_auto_splits_acc(int transA, int transB, int64_t m, int64_t n, int64_t k,
+                           const double *A, int64_t lda, const double *B, int64_t ldb,
+                           double tau, int s_max, int *capped)
+{
+    if (k < 1 || s_max < 1 || s_max > 64 || !(tau > 0.0)) return -1;
+    int w = oz_ref_slice_width(k);
+    double ra[65], rb[65];
+    if (oz_ref_trunc_residual(transA == 0 ? 0 : 1, m, k, A, lda, w, s_max, ra)) return -1;
+    if (oz_ref_trunc_residual(transB == 0 ? 1 : 0, n, k, B, ldb, w, s_max, rb)) return -1;
+    double target = tau * ldexp(sqrt((double)k), -53);
+    if (capped) *capped = 0;
+    for (int s = 1; s <= s_max; ++s)
+        if (oz_ref_acc_eta(ra, rb, s) <= target) return s;
+    if (capped) *capped = 1;
+    return s_max;
+}
