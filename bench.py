@@ -349,7 +349,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slices", type=int, default=None,
                     help="fixed s; 0 = INT8-AUTO with --auto-T (P:656-659)")
+    ap.add_argument("--auto-rule", default="acc", choices=["acc", "loss"],
+                    help="INT8-AUTO rule for --slices 0: acc = accuracy-targeted (reading A18, "
+                         "default), loss = the paper's mean-mantissa-loss rule (reading A17)")
     ap.add_argument("--auto-T", type=float, default=0.0)
+    ap.add_argument("--auto-tau", type=float, default=1.0)
     ap.add_argument("--chunk-cols", type=int, default=2048)
     ap.add_argument("--grid", default=None,
                     help="PRxPC: 2-D partition of C over the N ranks (SURVEY s8e 'large n'); "
@@ -422,7 +426,10 @@ def main():
     stream = torch.cuda.current_stream(dev)
     h.set_stream(stream)
     if s == 0:
-        h.set_auto(args.auto_T, 20)
+        if args.auto_rule == "loss":
+            h.set_auto(args.auto_T, 18)
+        else:
+            h.set_auto_accuracy(args.auto_tau, 18)
     be = D.CudaBackend(h, dev, reserve_sms=RESERVE_SMS if world > 1 else 0)
     bufs = None
 
@@ -448,7 +455,10 @@ def main():
     torch.cuda.synchronize()
     rep = h.report()
     if s == 0:
-        wl["auto"] = {"T": args.auto_T, "chosen_s": rep["num_slices"]}
+        wl["auto"] = {"rule": args.auto_rule,
+                      ("T" if args.auto_rule == "loss" else "tau"):
+                          (args.auto_T if args.auto_rule == "loss" else args.auto_tau),
+                      "chosen_s": rep["num_slices"], "capped": bool(rep["auto_capped"])}
         s = rep["num_slices"]  # for the op counts below; every timed step re-runs the scan
 
     # ---- timed region: inputs resident in HBM -------------------------------------
@@ -477,7 +487,8 @@ def main():
 
     # ---- dominant kernel: the fused GEMM (per-launch CUDA events on our stream) --------
     gemm_ms = float(np.mean([p["gemm_ms"] for p in phases])) if phases else None
-    slice_ms = float(np.mean([p["slice_a_ms"] + p["slice_b_ms"] for p in phases])) if phases else None
+    # A and B are sliced concurrently (two streams): the phase lasts max(start->A, start->B)
+    slice_ms = float(np.mean([max(p["slice_a_ms"], p["slice_b_ms"]) for p in phases])) if phases else None
     peaks, peak_src = load_peaks()
     int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     # one library GEMM call = the whole product at N = 1, one B column chunk at N > 1

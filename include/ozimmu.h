@@ -92,6 +92,10 @@ typedef struct {
     int k_chunks;          /* INT32-overflow-safe K chunks per tile (A4 budget) */
     int launches;          /* kernels launched by the last call */
     int acc_regions;       /* TMEM accumulator regions per level (INT32 sub-groups of pairs) */
+    int auto_mode;         /* 0: s given by the caller; OZIMMU_AUTO_LOSS / OZIMMU_AUTO_ACCURACY:
+                              s chosen by INT8-AUTO with that rule */
+    int auto_capped;       /* 1 if INT8-AUTO reached s_max without meeting its criterion (the
+                              result is then less accurate than the rule asked for) */
 } ozimmu_report_t;
 
 /* ---- handle ------------------------------------------------------------- */
@@ -123,8 +127,10 @@ OZIMMU_API ozimmu_status_t ozimmu_get_report(ozimmu_handle_t h, ozimmu_report_t 
 /* Per-phase device time of one computing call, from CUDA events the library records on
  * the handle's stream around each of its kernels (the paper's time breakdown). */
 typedef struct {
-    float slice_b_ms; /* A2+A3 on op(B) (0 for presliced calls) */
-    float slice_a_ms; /* A2+A3 on op(A) */
+    float slice_b_ms; /* call start -> op(B) sliced (A2+A3 on op(B); ~0 for presliced calls) */
+    float slice_a_ms; /* call start -> op(A) sliced.  ozimmu_dgemm slices op(B) on a second
+                         stream concurrently with op(A), so the slicing phase takes
+                         max(slice_a_ms, slice_b_ms); ozimmu_zgemm slices B then A */
     float gemm_ms;    /* A4+A5: the fused tcgen05 GEMM + epilogue kernel */
 } ozimmu_timing_t;
 /* Start recording phase events for the next `max_calls` computing calls (0 disables and
@@ -155,9 +161,10 @@ OZIMMU_API ozimmu_status_t ozimmu_dgemm(ozimmu_handle_t h, ozimmu_op_t transA, o
  * copies, the slicing of each chunk, the GEMM of each block and the D2H copy of each C
  * block run on three streams (the handle's stream + two internal copy streams), so tensor
  * work starts after the first chunk arrives.  C is bitwise identical to ozimmu_dgemm on the
- * same data.  num_slices = 0 (INT8-AUTO) copies both operands before choosing s (no
- * overlap).  Device memory: an internal buffer (grown on demand, freed by ozimmu_destroy)
- * of about s(n + 2 m/8) k_pad + 8 k (2 n/8 + 2 m/8) + 16 (m/8) n bytes.  The call BLOCKS
+ * same data.  num_slices = 0 (INT8-AUTO): op(A) row blocks and op(B) column chunks go H2D
+ * while the AUTO statistics of each landed block are computed; s is chosen once both operands
+ * are in, then C row blocks return while the next block's GEMM runs.  Device memory: an
+ * internal buffer (grown on demand, freed by ozimmu_destroy) of about s(n + 2 m/8) k_pad + 8 k (2 n/8 + 2 m/8) + 16 (m/8) n bytes.  The call BLOCKS
  * until C is in host memory.  Errors: as ozimmu_dgemm; WORKSPACE if the buffer cannot be
  * allocated. */
 OZIMMU_API ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t transA,
@@ -185,15 +192,33 @@ OZIMMU_API size_t ozimmu_zgemm_workspace_bytes(ozimmu_op_t transA, ozimmu_op_t t
                                     int64_t n, int64_t k, int num_slices);
 
 /* INT8-AUTO (NEXT row f2; "we select the number of splits so that the average
- * mantissa loss in the splitting process is equal to or smaller than a threshold T").
- * Reading A17: for a nonzero finite x of a row of op(A) / column of op(B) with exponent E,
- * the significant bits of |x|/2^E occupy positions lead = E - ilogb(x) .. t_last =
- * lead + vlen - 1 (vlen: bits from the MSB to the last 1 of the significand);
- * loss_s(x) = min(vlen, max(0, t_last - s*w)); s = the smallest s in [1, s_max] whose mean
- * loss over the nonzero finite elements is <= T for both operands (s_max if none).
- * ozimmu_set_auto sets T (>= 0, default 0) and s_max (default 20) for num_slices = 0 calls;
- * ozimmu_auto_splits returns the s such a call would use (synchronises the stream). */
+ * mantissa loss in the splitting process is equal to or smaller than a threshold T"): the
+ * splits are chosen per call by one of two rules; both scan every element of both operands
+ * on the device and read a few bytes back (the call synchronises its stream once).
+ *
+ * OZIMMU_AUTO_LOSS -- the paper's rule (reading A17): for a nonzero finite x of a row of
+ * op(A) / column of op(B) with exponent E, the significant bits of |x|/2^E occupy positions
+ * lead = E - ilogb(x) .. t_last = lead + vlen - 1 (vlen: bits from the MSB to the last 1 of
+ * the significand); loss_s(x) = min(vlen, max(0, t_last - s*w)); s = the smallest
+ * s in [1, s_max] whose mean loss over the nonzero finite elements is <= T for both operands.
+ * ozimmu_set_auto(h, T, s_max) selects it (T >= 0; T = 0 is the paper's lossless setting).
+ *
+ * OZIMMU_AUTO_ACCURACY (default) -- the k-aware rule the Discussion asks for (P:713-734:
+ * "the accumulation length should be one of the key factors"; reading A18): with rho_v(t)
+ * the relative l1 truncation residual of a vector after t digits (fixed-point upper estimate)
+ * and rho_A(t) / rho_B(t) its maximum over the rows of op(A) / columns of op(B), s = the
+ * smallest s in [1, s_max] with eta(s) = sum_{t=0..s} rho_A(t) rho_B(s-t) <= tau u sqrt(k)
+ * (u = 2^-53, k the accumulation length, 2k for ZGEMM's embedding): the predicted Ozaki error
+ * in units of |A||B| no larger than tau times FP64 DGEMM's probabilistic error level.
+ * ozimmu_set_auto_accuracy(h, tau, s_max) selects it (tau > 0; default tau = 1).
+ *
+ * s_max in [1, OZIMMU_MAX_SLICES], default 18; a call that reaches s_max without
+ * meeting its criterion sets ozimmu_report_t.auto_capped.  ozimmu_auto_splits returns the s a
+ * num_slices = 0 call would use (synchronises the stream). */
+#define OZIMMU_AUTO_LOSS 1
+#define OZIMMU_AUTO_ACCURACY 2
 OZIMMU_API ozimmu_status_t ozimmu_set_auto(ozimmu_handle_t h, double threshold, int s_max);
+OZIMMU_API ozimmu_status_t ozimmu_set_auto_accuracy(ozimmu_handle_t h, double tau, int s_max);
 OZIMMU_API ozimmu_status_t ozimmu_auto_splits(ozimmu_handle_t h, ozimmu_op_t transA,
                                    ozimmu_op_t transB, int64_t m, int64_t n, int64_t k,
                                    const double *A, int64_t lda, const double *B, int64_t ldb,

@@ -567,7 +567,12 @@ int oz_ref_trunc_residual(int trans, int64_t rows, int64_t kdim, const double *M
 {
     if (rows < 0 || kdim < 0 || s_max < 1 || s_max > 64 || w < 1) return OZR_ERR_ARG;
     for (int t = 0; t <= s_max; ++t) rho[t] = 0.0;
+    /* per-vector values (vectors are independent; the max below is order-free) */
+    double *rv = (double *)calloc((size_t)(rows > 0 ? rows : 1) * (size_t)(s_max + 1), sizeof(double));
+    if (!rv) return OZR_ERR_ARG;
+#pragma omp parallel for schedule(dynamic, 4)
     for (int64_t r = 0; r < rows; ++r) {
+        double *out = rv + r * (s_max + 1);
         double vmax = 0.0;
         int bad = 0;
         for (int64_t l = 0; l < kdim; ++l) {
@@ -575,7 +580,7 @@ int oz_ref_trunc_residual(int trans, int64_t rows, int64_t kdim, const double *M
             if (!isfinite(v)) bad = 1;
             else if (fabs(v) > vmax) vmax = fabs(v);
         }
-        if (bad || vmax == 0.0) continue;
+        if (bad || vmax == 0.0) continue; /* skipped: out stays 0 */
         int E;
         (void)frexp(vmax, &E);
         uint64_t D = 0, N[65];
@@ -586,12 +591,13 @@ int oz_ref_trunc_residual(int trans, int64_t rows, int64_t kdim, const double *M
             D += norm_dn32(v, E);
             for (int t = 1; t <= s_max; ++t) N[t] += resid_up32(v, E, w, t);
         }
-        rho[0] = 1.0;
-        for (int t = 1; t <= s_max; ++t) {
-            double q = ldexp((double)N[t] / (double)D, -w * t);
-            if (q > rho[t]) rho[t] = q;
-        }
+        out[0] = 1.0;
+        for (int t = 1; t <= s_max; ++t) out[t] = ldexp((double)N[t] / (double)D, -w * t);
     }
+    for (int64_t r = 0; r < rows; ++r)
+        for (int t = 0; t <= s_max; ++t)
+            if (rv[r * (s_max + 1) + t] > rho[t]) rho[t] = rv[r * (s_max + 1) + t];
+    free(rv);
     return OZR_OK;
 }
 

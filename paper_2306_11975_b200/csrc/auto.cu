@@ -215,7 +215,223 @@ __global__ void __launch_bounds__(256) k_loss_strided(const double *__restrict__
     hist_flush(H, out);
 }
 
+// ---- accuracy-targeted AUTO (reading A18, Discussion P:713-734) -------------------------
+// Per vector v with exponent E (rows of op(A) / columns of op(B)), over its nonzero finite
+// elements x, in 32-bit fixed point relative to 2^E:
+//     N_t(v) = sum ceil(frac(|x| 2^(wt-E)) 2^32)  (t = 1..s_max),  D(v) = sum floor(|x| 2^(32-E)),
+// exact integers (< 2^53: k <= 2^21 terms of <= 2^32), so the sums are order-free;
+// rho_v(t) = ((double)N_t / (double)D) 2^(-wt), and rho(t) = max over the vectors (the host
+// then takes the smallest s with sum_{t=0..s} rho_A(t) rho_B(s-t) <= tau u sqrt(k)).
+// With |x| = M 2^e0 (M the integer significand, e0 its exponent), |x| 2^(wt-E) = M 2^-z,
+// z = E - e0 - wt fraction bits: the residual after t digits is the low z bits of M.
+struct ResidAcc {
+    unsigned long long n[kMaxS + 1];  // [0] = D, [t] = N_t
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int t = 0; t <= kMaxS; ++t) n[t] = 0;
+    }
+    __device__ __forceinline__ void add(double x, int32_t E, int w, int s_max) {
+        const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+        const int be = static_cast<int>((u >> 52) & 0x7FF);
+        const uint64_t fr = u & ((1ull << 52) - 1);
+        const uint64_t M = be ? (fr | (1ull << 52)) : fr;
+        if (M == 0) return;
+        const int e0 = be ? be - 1075 : -1074;
+        const int z0 = E - e0;  // |x| / 2^E = M 2^-z0
+        // floor(M 2^(32 - z0)); for subnormal-only vectors z0 - 32 can be <= 0
+        const int sh = z0 - 32;
+        n[0] += sh <= 0 ? (M << (-sh)) : (sh >= 64 ? 0ull : (M >> sh));
+#pragma unroll
+        for (int t = 1; t <= kMaxS; ++t) {
+            if (t > s_max) break;
+            const int z = z0 - w * t;
+            uint64_t f;
+            if (z <= 0) {
+                f = 0;
+            } else {
+                const uint64_t R = z >= 64 ? M : (M & ((1ull << z) - 1));
+                if (z <= 32) {
+                    f = R << (32 - z);
+                } else {
+                    const int d = z - 32;  // ceil(R / 2^d): shift plus a sticky bit
+                    const uint64_t hi = d >= 64 ? 0ull : (R >> d);
+                    const uint64_t lo = d >= 64 ? R : (R & ((1ull << d) - 1));
+                    f = hi + (lo != 0 ? 1ull : 0ull);
+                }
+            }
+            n[t] += f;
+        }
+    }
+};
+
+// Contiguous vectors: persistent 256-thread blocks, one vector at a time (pass 1 exponent,
+// pass 2 the sums, block-reduced and written to sums[r][0..s_max]).
+__global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__ M, int64_t ld,
+                                                      int64_t rows, int64_t kdim, int w, int s_max,
+                                                      unsigned long long *__restrict__ sums,
+                                                      int32_t *__restrict__ keys_out) {
+    __shared__ int32_t kred[8];
+    __shared__ unsigned long long red[8][kMaxS + 1];
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const double *v = M + r * ld;
+        int32_t key = kKeyEmpty;
+        int64_t l = threadIdx.x;
+        for (; l + 3 * 256 < kdim; l += 4 * 256) {
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) key = max(key, exp_key_a(x[i]));
+        }
+        for (; l < kdim; l += 256) key = max(key, exp_key_a(__ldg(v + l)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
+        if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = key;
+        __syncthreads();
+        key = kred[0];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) key = max(key, kred[i]);
+        __syncthreads();  // kred is rewritten for the next vector
+        if (threadIdx.x == 0) keys_out[r] = key;
+        if (key == kExpNonFinite || key == kKeyEmpty) continue;  // skipped vector
+        ResidAcc acc;
+        acc.zero();
+        l = threadIdx.x;
+        for (; l + 3 * 256 < kdim; l += 4 * 256) {
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc.add(x[i], key, w, s_max);
+        }
+        for (; l < kdim; l += 256) acc.add(__ldg(v + l), key, w, s_max);
+#pragma unroll
+        for (int t = 0; t <= kMaxS; ++t) {
+            if (t > s_max) break;
+            unsigned long long x = acc.n[t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffff, x, o);
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][t] = x;
+        }
+        __syncthreads();
+        if (threadIdx.x <= (unsigned)s_max) {
+            unsigned long long x = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x += red[i][threadIdx.x];
+            sums[r * (s_max + 1) + threadIdx.x] = x;
+        }
+        __syncthreads();
+    }
+}
+
+// Strided vectors (element l of vector r at M[r + l ld]; complex: the (re, im) pair): one
+// thread per vector and a slice of l per blockIdx.y, partial sums added to sums[r][.]
+// (zeroed by the caller; integer atomics, so the totals do not depend on the order).
+template <int CPX>
+__global__ void __launch_bounds__(256) k_resid_strided(const double *__restrict__ M, int64_t ld,
+                                                       int64_t rows, int64_t kdim, int64_t lchunk,
+                                                       const int32_t *__restrict__ keys, int w,
+                                                       int s_max,
+                                                       unsigned long long *__restrict__ sums) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+    const int32_t key = r < rows ? keys[r] : kKeyEmpty;
+    if (key == kExpNonFinite || key == kKeyEmpty) return;
+    ResidAcc acc;
+    acc.zero();
+    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
+    const int64_t l1 = min(kdim, l0 + lchunk);
+    if (CPX) {
+        const double2 *Mc = reinterpret_cast<const double2 *>(M);
+        for (int64_t l = l0; l < l1; ++l) {
+            const double2 z = __ldg(Mc + r + l * ld);
+            acc.add(z.x, key, w, s_max);
+            acc.add(z.y, key, w, s_max);
+        }
+    } else {
+        int64_t l = l0;
+        for (; l + 4 <= l1; l += 4) {
+            double x[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) x[i] = __ldg(M + r + (l + i) * ld);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc.add(x[i], key, w, s_max);
+        }
+        for (; l < l1; ++l) acc.add(__ldg(M + r + l * ld), key, w, s_max);
+    }
+#pragma unroll
+    for (int t = 0; t <= kMaxS; ++t) {
+        if (t > s_max) break;
+        if (acc.n[t]) atomicAdd(&sums[r * (s_max + 1) + t], acc.n[t]);
+    }
+}
+
+// rho_v(t) per vector from its sums, max over the vectors into rho_out[0..s_max] (as the bit
+// patterns of non-negative doubles, whose unsigned order is their numeric order).
+__global__ void k_resid_rho(const unsigned long long *__restrict__ sums, const int32_t *__restrict__ keys,
+                            int64_t rows, int w, int s_max, unsigned long long *__restrict__ rho_out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.y + threadIdx.y;
+    const int t = threadIdx.x;
+    if (r >= rows || t > s_max) return;
+    const int32_t key = keys[r];
+    if (key == kExpNonFinite || key == kKeyEmpty) return;
+    double rho = 1.0;
+    if (t > 0) {
+        const double q = __ddiv_rn((double)sums[r * (s_max + 1) + t], (double)sums[r * (s_max + 1)]);
+        rho = __dmul_rn(q, __longlong_as_double(static_cast<long long>(1023 - w * t) << 52));
+    }
+    if (rho > 0.0) atomicMax(&rho_out[t], static_cast<unsigned long long>(__double_as_longlong(rho)));
+}
+
 }  // namespace
+
+// Accuracy-targeted AUTO statistics of the vectors of op(M): rho_out (device, s_max + 1 uint64
+// holding doubles; max-accumulated, caller zeroes it).  scratch: device uint64
+// [rows (s_max + 1)] + int32 [rows] keys.
+cudaError_t launch_trunc_residual(const double *M, int64_t ld, bool contiguous, int64_t rows,
+                                  int64_t kdim, int w, int s_max, unsigned long long *rho_out,
+                                  void *scratch, int num_sms, cudaStream_t st, int *launches,
+                                  int cpx) {
+    if (rows <= 0 || kdim <= 0) return cudaSuccess;
+    if (s_max < 1 || s_max > kMaxS || w < 1 || w > 7) return cudaErrorInvalidValue;
+    unsigned long long *sums = static_cast<unsigned long long *>(scratch);
+    int32_t *keys = reinterpret_cast<int32_t *>(sums + rows * (s_max + 1));
+    cudaError_t e;
+    if (contiguous) {
+        int64_t blocks = 4 * (int64_t)num_sms;
+        if (blocks > rows) blocks = rows;
+        k_resid_contig<<<(unsigned)blocks, 256, 0, st>>>(M, ld, rows, kdim, w, s_max, sums, keys);
+        ++*launches;
+    } else {
+        e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * rows * (s_max + 1), st);
+        if (e != cudaSuccess) return e;
+        e = launch_expscan(M, ld, rows, kdim, keys, num_sms, st, launches, cpx);
+        if (e != cudaSuccess) return e;
+        const int64_t rblocks = ceil_div(rows, 256);
+        int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
+        if (ysplit < 1) ysplit = 1;
+        int64_t lchunk = ceil_div(kdim, ysplit);
+        if (lchunk < 256) lchunk = 256;
+        ysplit = ceil_div(kdim, lchunk);
+        if (cpx)
+            k_resid_strided<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+                M, ld, rows, kdim, lchunk, keys, w, s_max, sums);
+        else
+            k_resid_strided<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+                M, ld, rows, kdim, lchunk, keys, w, s_max, sums);
+        ++*launches;
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int ty = 256 / 64;  // 64 threads (t = 0..s_max) x 4 vectors per block
+    k_resid_rho<<<(unsigned)ceil_div(rows, ty), dim3(64, ty), 0, st>>>(sums, keys, rows, w, s_max,
+                                                                       rho_out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+size_t trunc_residual_scratch(int64_t rows, int s_max) {
+    return sizeof(unsigned long long) * (size_t)rows * (s_max + 1) + sizeof(int32_t) * (size_t)rows;
+}
 
 // out: device uint64 [kMaxS + 1] (loss sums for s = 1..s_max, then the nonzero count),
 // accumulated (caller zeroes it).  key_scratch: int32 [rows] (strided case).  cpx: the

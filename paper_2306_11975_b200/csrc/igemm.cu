@@ -120,6 +120,16 @@ size_t chunk_scratch_bytes(const GemmPlan &p, int s) {
     return (size_t)p.grid * s * p.tile_n * kBlockM * sizeof(int64_t);
 }
 
+// Upper bound of chunk_scratch_bytes over every SM cap (ozimmu_set_max_sms) and device of up to
+// max_sms SMs: the tile width may switch between 32 and nc_for(s) with the cap (small-problem
+// rule in plan_gemm), and the grid is at most max_sms CTAs.
+size_t chunk_scratch_bound(const GemmPlan &p, int s, int max_sms) {
+    if (p.k_chunks <= 1) return 0;
+    const int nc = nc_for(s) > p.tile_n ? nc_for(s) : p.tile_n;
+    const int g = p.grid > max_sms ? p.grid : max_sms;
+    return (size_t)g * s * nc * kBlockM * sizeof(int64_t);
+}
+
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st,
                         int *launches) {
     if (a.m <= 0 || a.n <= 0) return cudaSuccess;

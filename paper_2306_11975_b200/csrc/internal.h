@@ -59,6 +59,15 @@ cudaError_t launch_mantissa_loss(const double *M, int64_t ld, bool contiguous, i
                                  int32_t *key_scratch, int num_sms, cudaStream_t st,
                                  int *launches, int cpx = 0);
 
+// ---- accuracy-targeted INT8-AUTO statistics (f2, reading A18) ----------------------------
+// rho_out: device uint64 [s_max + 1] holding non-negative doubles, max-accumulated (zero it
+// first); scratch: trunc_residual_scratch(rows, s_max) bytes of device memory.
+cudaError_t launch_trunc_residual(const double *M, int64_t ld, bool contiguous, int64_t rows,
+                                  int64_t kdim, int w, int s_max, unsigned long long *rho_out,
+                                  void *scratch, int num_sms, cudaStream_t st, int *launches,
+                                  int cpx = 0);
+size_t trunc_residual_scratch(int64_t rows, int s_max);
+
 // ---- fused GEMM (A4 + A5) ----------------------------------------------------------------
 enum EpiMode : int { EPI_DGEMM = 0, EPI_LEVELS_I64 = 1, EPI_PAIR_I32 = 2, EPI_ZGEMM = 3 };
 
@@ -100,6 +109,7 @@ struct GemmPlan {
 // Choose tile/pipeline parameters for (s, w, k_pad); returns false if unsupported.
 bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, GemmPlan *p);
 size_t chunk_scratch_bytes(const GemmPlan &p, int s);
+size_t chunk_scratch_bound(const GemmPlan &p, int s, int max_sms);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st,
                         int *launches);
 

@@ -30,7 +30,10 @@ EXPORTS = [
     "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
     "ozimmu_set_auto", "ozimmu_auto_splits", "ozimmu_dgemm_strided_batched",
     "ozimmu_zgemm_strided_batched", "ozimmu_dgemm_host", "ozimmu_set_max_sms",
+    "ozimmu_set_auto_accuracy",
 ]
+AUTO_LOSS, AUTO_ACCURACY = 1, 2
+AUTO_SMAX_DEFAULT = 18
 
 
 class OzimmuError(RuntimeError):
@@ -48,7 +51,7 @@ class Report(ct.Structure):
                 ("gemm_pairs", ct.c_int64), ("int8_macs", ct.c_int64),
                 ("slice_bytes", ct.c_int64), ("tile_n", ct.c_int), ("k_block", ct.c_int),
                 ("stages", ct.c_int), ("k_chunks", ct.c_int), ("launches", ct.c_int),
-                ("acc_regions", ct.c_int)]
+                ("acc_regions", ct.c_int), ("auto_mode", ct.c_int), ("auto_capped", ct.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -91,6 +94,7 @@ def lib():
         "ozimmu_zgemm": ([H, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, i32], i32),
         "ozimmu_zgemm_workspace_bytes": ([i32, i32, i64, i64, i64, i32], sz),
         "ozimmu_set_auto": ([H, ct.c_double, i32], i32),
+        "ozimmu_set_auto_accuracy": ([H, ct.c_double, i32], i32),
         "ozimmu_dgemm_strided_batched": ([H, i32, i32, i64, i64, i64, dp, vp, i64, i64, vp, i64,
                                           i64, dp, vp, i64, i64, i64, i32], i32),
         "ozimmu_zgemm_strided_batched": ([H, i32, i32, i64, i64, i64, dp, vp, i64, i64, vp, i64,
@@ -217,9 +221,16 @@ class Handle:
             self._h, OP[transA], OP[transB], m, n, k, _d(alpha), _hptr(A), lda, _hptr(B), ldb,
             _d(beta), _hptr(C), ldc, int(num_slices)))
 
-    def set_auto(self, threshold, s_max=20):
-        """INT8-AUTO settings for num_slices = 0 calls."""
+    def set_auto(self, threshold, s_max=AUTO_SMAX_DEFAULT):
+        """INT8-AUTO with the paper's mean-mantissa-loss rule (reading A17) for
+        num_slices = 0 calls."""
         _check("ozimmu_set_auto", lib().ozimmu_set_auto(self._h, float(threshold), int(s_max)))
+
+    def set_auto_accuracy(self, tau=1.0, s_max=AUTO_SMAX_DEFAULT):
+        """INT8-AUTO with the k-aware accuracy-targeted rule (reading A18, the default):
+        predicted error <= tau x FP64 DGEMM's probabilistic error level."""
+        _check("ozimmu_set_auto_accuracy",
+               lib().ozimmu_set_auto_accuracy(self._h, float(tau), int(s_max)))
 
     def auto_splits(self, transA, transB, m, n, k, A, lda, B, ldb):
         out = ct.c_int()

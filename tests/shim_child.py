@@ -26,7 +26,18 @@ def main(out):
     Bb = np.ascontiguousarray(np.stack([synth.gen_phi(bk, bn, 1.0, 20 + b) for b in range(batch)]))
     Cb = torch.bmm(torch.from_numpy(Ab).cuda(), torch.from_numpy(Bb).cuda())
     torch.cuda.synchronize()
-    np.savez(out, C=C.cpu().numpy(), Cz=Cz.cpu().numpy(), Cb=Cb.cpu().numpy())
+    # the shim's own counters (present only when it is preloaded)
+    counters = np.array([-1, -1], dtype=np.int64)
+    try:
+        import ctypes as ct
+        fn = ct.CDLL(None).ozimmu_shim_counters
+        a, b = ct.c_longlong(), ct.c_longlong()
+        fn(ct.byref(a), ct.byref(b))
+        counters = np.array([a.value, b.value], dtype=np.int64)
+    except (AttributeError, OSError):
+        pass
+    np.savez(out, C=C.cpu().numpy(), Cz=Cz.cpu().numpy(), Cb=Cb.cpu().numpy(),
+             counters=counters)
 
 
 if __name__ == "__main__":

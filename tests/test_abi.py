@@ -76,8 +76,8 @@ def test_null_handle_validation():
 
 
 def test_cublas_shim_exports():
-    """NEXT row f3: the LD_PRELOAD shim defines exactly the cuBLAS GEMMs it interposes and
-    loads without a GPU (resolving libozimmu.so next to itself)."""
+    """NEXT row f3: the LD_PRELOAD shim defines exactly the cuBLAS GEMMs it interposes (plus its
+    counters) and loads without a GPU (resolving libozimmu.so next to itself)."""
     import ctypes
     import subprocess
     shim = os.path.join(os.path.dirname(B.__file__), "libozimmu_cublas_shim.so")
@@ -86,5 +86,8 @@ def test_cublas_shim_exports():
                          check=True).stdout
     defined = sorted(l.split()[-1] for l in out.splitlines() if " T " in l)
     assert defined == sorted(["cublasDgemm_v2", "cublasZgemm_v2", "cublasDgemmStridedBatched",
-                              "cublasZgemmStridedBatched"])
-    ctypes.CDLL(shim)
+                              "cublasZgemmStridedBatched", "ozimmu_shim_counters"])
+    L = ctypes.CDLL(shim)
+    a, b = ctypes.c_longlong(7), ctypes.c_longlong(7)
+    L.ozimmu_shim_counters(ctypes.byref(a), ctypes.byref(b))
+    assert (a.value, b.value) == (0, 0)

@@ -42,7 +42,15 @@ def _col(X):
     return np.asfortranarray(np.asarray(X).T)
 
 
-def _check_calls(res, calls, fixed_s):
+def _s_auto(ta, tb, m, n, k, A, lda, B, ldb, mode):
+    """The oracle's INT8-AUTO choice under the shim's rule (mode 'acc' = reading A18, the
+    default; 'loss' = the paper's T = 0 rule, reading A17)."""
+    if mode == "loss":
+        return O.auto_splits(ta, tb, m, n, k, A, lda, B, ldb, 0.0, 18)
+    return O.auto_splits_acc(ta, tb, m, n, k, A, lda, B, ldb, 1.0, 18)[0]
+
+
+def _check_calls(res, calls, fixed_s, mode="acc"):
     assert [c[0] for c in calls] == ["cublasDgemm_v2", "cublasZgemm_v2",
                                      "cublasDgemmStridedBatched"], calls
     # row-major C = A B reaches cuBLAS as C^T = B^T A^T: ta = tb = N, (m, n) swapped
@@ -56,7 +64,7 @@ def _check_calls(res, calls, fixed_s):
     if fixed_s:
         assert s == fixed_s
     else:
-        assert s == O.auto_splits("N", "N", n, m, k, _col(B), n, _col(A), k, 0.0, 20)
+        assert s == _s_auto("N", "N", n, m, k, _col(B), n, _col(A), k, mode)
     ref = O.dgemm("N", "N", n, m, k, 1.0, _col(B), n, _col(A), k, 0.0,
                   np.zeros((n, m), order="F"), n, s)
     assert np.array_equal(res["C"], ref.T)
@@ -74,10 +82,12 @@ def _check_calls(res, calls, fixed_s):
     assert (int(cm), int(cn), int(ck), int(cb)) == (bn, bm, bk, batch)
     for b in range(batch):
         Ab, Bb = synth.gen_phi(bm, bk, 1.0, 10 + b), synth.gen_phi(bk, bn, 1.0, 20 + b)
-        sb = fixed_s or O.auto_splits("N", "N", bn, bm, bk, _col(Bb), bn, _col(Ab), bk, 0.0, 20)
+        sb = fixed_s or _s_auto("N", "N", bn, bm, bk, _col(Bb), bn, _col(Ab), bk, mode)
         ref = O.dgemm("N", "N", bn, bm, bk, 1.0, _col(Bb), bn, _col(Ab), bk, 0.0,
                       np.zeros((bn, bm), order="F"), bn, sb)
         assert np.array_equal(res["Cb"][b], ref.T), b
+    # every intercepted call ran on libozimmu: nothing fell through to cuBLAS
+    assert list(res["counters"]) == [3, 0], res["counters"]
 
 
 def test_shim_fixed_slices(tmp_path):
@@ -86,15 +96,36 @@ def test_shim_fixed_slices(tmp_path):
 
 
 def test_shim_int8_auto(tmp_path):
-    """Default: INT8-AUTO with T = 0 (the paper's lossless setting)."""
+    """Default: INT8-AUTO with the accuracy-targeted rule (reading A18, tau = 1)."""
     env = {"OZIMMU_SHIM_LOG": "1"}
     res, calls = _run(tmp_path, env)
-    _check_calls(res, calls, None)
+    _check_calls(res, calls, None, "acc")
+
+
+def test_shim_int8_auto_loss_rule(tmp_path):
+    """OZIMMU_SHIM_AUTO=loss: the paper's rule with T = 0 (the lossless setting)."""
+    res, calls = _run(tmp_path, {"OZIMMU_SHIM_LOG": "1", "OZIMMU_SHIM_AUTO": "loss"})
+    _check_calls(res, calls, None, "loss")
+
+
+def test_shim_counts_fall_through(tmp_path):
+    """A call libozimmu rejects (s > OZIMMU_MAX_SLICES) goes to cuBLAS, is counted and is
+    reported on stderr -- never silent."""
+    out = str(tmp_path / "out.npz")
+    env = dict(os.environ)
+    env.update({"OZIMMU_SHIM_SLICES": "99", "LD_PRELOAD": SHIM})
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "shim_child.py"), out, ROOT],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = np.load(out)
+    assert list(res["counters"]) == [0, 3], res["counters"]
+    assert "WARNING cublasDgemm_v2 ran on cuBLAS FP64 instead" in r.stderr
 
 
 def test_shim_disabled_forwards_to_cublas(tmp_path):
     res, calls = _run(tmp_path, {"OZIMMU_SHIM_LOG": "1", "OZIMMU_SHIM_DISABLE": "1"})
     assert calls == []
+    assert list(res["counters"]) == [0, 3]
     m, n, k = 96, 80, 200
     A, B = synth.gen_phi(m, k, 1.0, 1), synth.gen_phi(k, n, 1.0, 2)
     ref = A @ B
