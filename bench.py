@@ -144,6 +144,17 @@ class ClockSampler:
                 "power_w_median": float(np.median(power))}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline_sample(A, B, k, s, target_s=15.0):
     """Time the oracle (as it stands, test infrastructure) on a bounded sample of the
     workload: `rows` rows x `cols` columns of C (rows of A / columns of B gathered whole,
@@ -241,7 +252,7 @@ def run_reference(args, wl):
             "config": {"workload": wl["desc"], "m": m, "n": n, "k": k, "s": s, "phi": wl["phi"],
                        "parallelism": "cpu oracle, OpenMP"},
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -340,6 +351,21 @@ def run_zgemm(args, wl):
     h.close()
 
 
+def self_launch(args):
+    """`bench.py --gpus N` without torchrun: start N ranks (one per GPU) with
+    torch.distributed.run on 127.0.0.1 and return its exit code; refuse loudly if fewer than N
+    GPUs are visible (OZIMMU_BENCH_ONE_DEVICE=1: the one-GPU test hook, all ranks on cuda:0)."""
+    import torch
+    ndev = torch.cuda.device_count()
+    if os.environ.get("OZIMMU_BENCH_ONE_DEVICE") != "1" and ndev < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {ndev} CUDA device(s) are "
+                         "visible; refusing to report a multi-GPU number from fewer GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--local-addr", "127.0.0.1",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -354,7 +380,11 @@ def main():
                          "default), loss = the paper's mean-mantissa-loss rule (reading A17)")
     ap.add_argument("--auto-T", type=float, default=0.0)
     ap.add_argument("--auto-tau", type=float, default=1.0)
-    ap.add_argument("--chunk-cols", type=int, default=2048)
+    ap.add_argument("--chunk-cols", type=int, default=0,
+                    help="N > 1: columns per broadcast chunk (0 = the library's default, ~n/8)")
+    ap.add_argument("--bcast-fp64", action="store_true",
+                    help="N > 1: broadcast FP64 B and slice it on every rank (SURVEY s8e byte "
+                         "trade-off) instead of B's INT8 planes")
     ap.add_argument("--grid", default=None,
                     help="PRxPC: 2-D partition of C over the N ranks (SURVEY s8e 'large n'); "
                          "default: row blocks")
@@ -369,6 +399,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, wl)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if wl.get("complex"):
         run_zgemm(args, wl)
         return
@@ -383,25 +415,23 @@ def main():
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
     # test hook (never set by the driver): OZIMMU_BENCH_ONE_DEVICE=1 maps every rank to cuda:0
-    # and uses gloo, so the N > 1 code path can be exercised on a one-GPU box (timings
-    # meaningless: the ranks share one GPU and gloo stages through the host)
+    # and broadcasts over gloo (NCCL refuses two ranks on one GPU), so the N > 1 code path can
+    # run on a one-GPU box (timings meaningless: the ranks share one GPU)
     one_dev = os.environ.get("OZIMMU_BENCH_ONE_DEVICE") == "1"
     if one_dev:
         local = 0
+    torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        if one_dev:
-            dist.init_process_group("gloo")
-        else:
-            # the broadcast kernels run on SMs the GEMM leaves free (dist.CudaBackend)
-            os.environ.setdefault("NCCL_MAX_CTAS", str(RESERVE_SMS))
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
+        # torch.distributed (gloo) is only the bootstrap: the NCCL unique id, barriers and the
+        # max-over-ranks of the timings.  The broadcast itself is libozimmu's NCCL communicator.
+        dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     m, n, k, s = wl["m"], wl["n"], wl["k"], wl["s"]
-    s_call = s  # 0 = INT8-AUTO: every step runs the mantissa-loss scan
+    if world > 1 and s == 0:
+        raise SystemExit("bench.py: INT8-AUTO (--slices 0) is single-GPU only (choosing s would "
+                         "need A's statistics from every rank)")
+    s_call = s  # 0 = INT8-AUTO: every step runs the statistics scan
     pr, pc = world, 1
     if args.grid and world > 1:
         pr, pc = (int(x) for x in args.grid.lower().split("x"))
@@ -410,7 +440,6 @@ def main():
     r0, r1 = D.row_range(m, pr, gi)
     n0, n1 = D.row_range(n, pc, gj)
     ml, nl = r1 - r0, n1 - n0
-    groups = D.make_grid_groups(pr, pc, 0) if pc > 1 else None
 
     # ---- inputs (identical bytes to the oracle's: synth.gen_phi) ------------------
     A = synth.gen_phi(m, k, wl["phi"], wl["seeds"][0])
@@ -419,7 +448,7 @@ def main():
     B_h = torch.from_numpy(B.ravel(order="F")) if B is not None else None
     dA = A_loc_h.to(dev)
     dB = B_h.to(dev) if B_h is not None else None
-    dC = torch.empty(ml * nl, dtype=torch.float64, device=dev)
+    dC = torch.empty(max(1, ml * nl), dtype=torch.float64, device=dev)
     lda = max(1, ml)
 
     h = oz.Handle(local)
@@ -430,21 +459,28 @@ def main():
             h.set_auto(args.auto_T, 18)
         else:
             h.set_auto_accuracy(args.auto_tau, 18)
-    be = D.CudaBackend(h, dev, reserve_sms=RESERVE_SMS if world > 1 else 0)
-    bufs = None
+    engine = engines = None
+    if world > 1:
+        h.set_dist(args.chunk_cols, RESERVE_SMS, args.bcast_fp64)
+        if one_dev:
+            make = lambda g, mem: D.BcastEngine(h, g, mem)  # noqa: E731
+        else:
+            def make(g, mem):
+                return D.NcclEngine(h, D.make_nccl_comm(local, g, RESERVE_SMS, mem))
+        if pc > 1:
+            engines = D.make_grid_engines(make, pr, pc, 0)
+        else:
+            engine = make(None, list(range(world)))
 
     def step():
-        nonlocal bufs
         if world == 1:
             h.dgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, s_call)
-        elif groups is not None:
-            bufs = D.dgemm_grid2d(be, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0, dC, lda,
-                                  s_call, pr, pc, groups, root=0, chunk_cols=args.chunk_cols,
-                                  bufs=bufs)
+        elif engines is not None:
+            D.dgemm_grid2d(engines, pr, pc, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0, dC, lda,
+                           s_call, root=0)
         else:
-            bufs = D.dgemm_rowblock(be, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0,
-                                    dC.view(n, ml).t() if ml else dC, lda, s_call, root=0,
-                                    chunk_cols=args.chunk_cols, bufs=bufs)
+            D.dgemm_rowblock(engine, "N", "N", ml, n, k, 1.0, dA, lda, dB, k, 0.0, dC, lda,
+                             s_call, root=0)
 
     def barrier():
         if world > 1:
@@ -478,12 +514,27 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     phases = h.timing_read(args.steps + 1)
     h.timing_enable(0)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
+    if world > 1:  # max over ranks (gloo: CPU tensor)
+        t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     flops = 2.0 * m * n * k
     value = flops / (ms / 1e3) / 1e12
+    bcast = None
+    if world > 1 and phases:
+        # the library marks the end of the last broadcast on its collective stream: start ->
+        # last chunk received, and the payload this rank received (INT8 planes + exponents, or
+        # FP64 B); SURVEY s8e byte trade-off: s vs 8 bytes per element of op(B)
+        k_pad = (k + 15) // 16 * 16
+        payload = (8 * k * nl) if (args.bcast_fp64) else (s * nl * k_pad + 4 * nl)
+        t_b = float(np.mean([p["slice_b_ms"] for p in phases]))
+        bcast = {"payload_bytes_per_rank": int(payload), "ms_start_to_last_chunk": t_b,
+                 "gbps_effective": payload / (t_b / 1e3) / 1e9 if t_b > 0 else None,
+                 "payload": "fp64 op(B)" if args.bcast_fp64 else "INT8 planes + exponents",
+                 "chunk_cols": args.chunk_cols or "library default (~n/8)",
+                 "reserve_sms": RESERVE_SMS, "nccl_max_ctas": RESERVE_SMS,
+                 "transport": "gloo host-staged (one-device test hook)" if one_dev
+                 else "NCCL (libozimmu's communicator)"}
 
     # ---- dominant kernel: the fused GEMM (per-launch CUDA events on our stream) --------
     gemm_ms = float(np.mean([p["gemm_ms"] for p in phases])) if phases else None
@@ -491,8 +542,9 @@ def main():
     slice_ms = float(np.mean([max(p["slice_a_ms"], p["slice_b_ms"]) for p in phases])) if phases else None
     peaks, peak_src = load_peaks()
     int8_peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    # one library GEMM call = the whole product at N = 1, one B column chunk at N > 1
-    n_launch = n if world == 1 else min(args.chunk_cols, nl)
+    # N = 1: one GEMM launch per call; N > 1: gemm_ms spans this rank's GEMM launches of a
+    # call (1, 1, 2, 4, .. column chunks each), so the ops are all of the rank's block
+    n_launch = n if world == 1 else nl
     int8_ops_launch = float(s * (s + 1)) * ml * n_launch * k  # 2 ops per INT8 MAC
     achieved = int8_ops_launch / (gemm_ms / 1e3) / 1e12 if gemm_ms else None
     traffic = None
@@ -516,8 +568,8 @@ def main():
                 "tensor_util_at_measured_clock": (achieved / hw_at_clock)
                 if (achieved and hw_at_clock) else None,
                 "ops_per_launch": int8_ops_launch,
-                "ops": "INT8 ops (2 per MAC) = s(s+1) m_loc n_launch k (n_launch = n at N = 1, "
-                       "one B chunk at N > 1)",
+                "ops": "INT8 ops (2 per MAC) = s(s+1) m_loc n_loc k over the GEMM span of a call "
+                       "(one launch at N = 1)",
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json; {INT8_PEAK_NOTE}",
                 "gemm_ms": gemm_ms, "slice_ms": slice_ms,
                 "gemm_share_of_step": (gemm_ms / ms) if gemm_ms else None,
@@ -526,9 +578,9 @@ def main():
     # ---- cuBLAS DGEMM on the same GPUs (row block, B resident: no communication) -----
     cublas = None
     if not args.no_cublas:
-        Bt = dB if dB is not None else torch.empty(k * n, dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.broadcast(Bt, src=0)
+        # non-root ranks regenerate B (same seed) instead of receiving it: no communication
+        Bt = dB if dB is not None else torch.from_numpy(
+            synth.gen_phi(k, n, wl["phi"], wl["seeds"][1]).ravel(order="F")).to(dev)
         Am = dA.view(k, ml).t() if ml else None
         Bm = Bt.view(n, k).t()[:, n0:n1]
         Cm = torch.empty(ml, nl, dtype=torch.float64, device=dev)
@@ -547,14 +599,15 @@ def main():
         torch.cuda.synchronize()
         cms = e0.elapsed_time(e1) / max(3, args.steps // 2)
         if world > 1:
-            t = torch.tensor([cms], device=dev)
+            t = torch.tensor([cms], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             cms = float(t.item())
         cv = flops / (cms / 1e3) / 1e12
         cublas = {"value": cv, "unit": "TFLOP/s", "ms_per_step": cms,
                   "frac_of_fp64_peak_40": cv / 40.0 / world, "speedup_ozimmu_vs_cublas": value / cv,
                   "note": "torch.matmul float64 (cuBLAS DGEMM), same C blocks, B already resident"}
-        del Cm
+        if world > 1 or args.no_cpu_baseline:
+            del Cm
         if world > 1:
             del Bt
 
@@ -591,7 +644,7 @@ def main():
         wall = (time.perf_counter() - t0) / esteps * 1e3
         ems = e0.elapsed_time(e1) / esteps
         if world > 1:
-            t = torch.tensor([ems, wall], device=dev)
+            t = torch.tensor([ems, wall], dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems, wall = float(t[0].item()), float(t[1].item())
         same = None
@@ -621,7 +674,7 @@ def main():
         torch.cuda.synchronize()
         cv_, dt_, desc, (rows, cols, Cs) = cpu_baseline_sample(A, B, k, s)
         cpu = {"value": cv_, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": desc, "seconds": dt_}
+               "sample": desc, "seconds": dt_, "cpu_model": cpu_model()}
         ph = cpu_phase_breakdown(A, B, k, s, rows, cols)
         ph["accumulate_s"] = max(0.0, dt_ - ph["split_s"] - ph["pair_products_s"])
         ph["note"] = ("oracle phases on the same sample (P:613-620 Fig. 9 split): accumulate = "
@@ -633,18 +686,40 @@ def main():
         hi, lo = O.dd_gemm("N", "N", len(rows), len(cols), k, np.asfortranarray(A[rows]),
                            len(rows), np.asfortranarray(B[:, cols]), k)
         st = O.err_stats(Cg, hi, lo)
+        # condition of each sampled output, (|A||B|)_ij / |C_ij| (the literal max_rel is driven
+        # by huge ones); the diagnostic restricts max_rel to cond <= 4 x median
+        absAB = np.abs(A[rows]) @ np.abs(B[:, cols])
+        cond = absAB / np.maximum(np.abs(hi), np.finfo(float).tiny)
+        well = cond <= 4.0 * np.median(cond)
+        ref_abs = np.abs(hi)
+
+        def cond_max_rel(Cx):
+            d = np.abs((Cx - hi) - lo)
+            sel = well & (ref_abs > 0)
+            return float((d[sel] / ref_abs[sel]).max()) if sel.any() else None
         accuracy = {"vs": "double-double (oracle/dd_ref.c) on the cpu_baseline sample",
                     "max_rel": st["max_rel"], "mean_rel": st["mean_rel"], "nw_max": st["nw_max"],
-                    "bitexact_vs_oracle": bool(np.array_equal(Cg, Cs)),
-                    "gate": "nw_max <= 1e-14 and mean_rel <= 1e-14 (SURVEY s8c reading)"}
+                    "max_rel_cond_le_4x_median": cond_max_rel(Cg),
+                    "cond_median": float(np.median(cond)), "cond_max": float(cond.max()),
+                    "bitexact_vs_oracle": bool(np.array_equal(Cg, Cs))}
+        if cublas is not None:  # cuBLAS DGEMM's full-size result on the same sample
+            Cc = Cm[torch.as_tensor(rows, device=dev)][:, torch.as_tensor(cols, device=dev)]
+            Cc = Cc.cpu().numpy()
+            sc = O.err_stats(Cc, hi, lo)
+            accuracy["cublas"] = {"max_rel": sc["max_rel"], "mean_rel": sc["mean_rel"],
+                                  "nw_max": sc["nw_max"],
+                                  "max_rel_cond_le_4x_median": cond_max_rel(Cc)}
+            del Cm
+        mr_cub = accuracy.get("cublas", {}).get("mean_rel")
+        accuracy["gate"] = ("nw_max <= 1e-14 and mean_rel <= min(1e-14, cuBLAS mean_rel) "
+                            "(SURVEY s8c reading A14)")
+        accuracy["gate_pass"] = bool(st["nw_max"] <= 1e-14 and st["mean_rel"] <= 1e-14 and
+                                     (mr_cub is None or st["mean_rel"] <= mr_cub))
 
     launches_per_step = rep.get("launches", 0)
-    if world > 1:
-        # rank 0's count: it slices every B chunk (one launch each) and runs its own chunks
-        nch = len(D.col_chunks(nl, args.chunk_cols))
-        nall = sum(len(D.col_chunks(b - a, args.chunk_cols))
-                   for a, b in (D.row_range(n, pc, jj) for jj in range(pc)))
-        launches_per_step = nch * (rep.get("launches", 0)) + (nall if rank == 0 else 0)
+    if world > 1:  # rank 0's kernels per step (its slicing of every B chunk included)
+        engs = [e for e in (engines or [engine]) if e is not None]
+        launches_per_step = sum(e.launches for e in engs)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -668,6 +743,7 @@ def main():
         "clocks": clk,
         "gpu_launches": int(launches_per_step * args.steps),
         "phases_ms_mean": {"slice": slice_ms, "gemm": gemm_ms},
+        "bcast": bcast,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

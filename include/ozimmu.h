@@ -75,7 +75,9 @@ typedef enum {
     OZIMMU_ERR_UNSUPPORTED = 2,   /* valid BLAS call outside what is implemented (s = 0, k too large) */
     OZIMMU_ERR_WORKSPACE = 3,     /* caller workspace too small / allocation failed */
     OZIMMU_ERR_CUDA = 4,          /* a CUDA runtime/driver call or launch failed */
-    OZIMMU_ERR_NOT_INITIALIZED = 5
+    OZIMMU_ERR_NOT_INITIALIZED = 5, /* NULL handle */
+    OZIMMU_ERR_NCCL = 6           /* NCCL could not be loaded, or an NCCL call / the caller's
+                                     broadcast function failed (multi-GPU entry points) */
 } ozimmu_status_t;
 
 /* Per-call report of the last computing call on a handle (SPEC GemmReport, S:378-381;
@@ -261,6 +263,61 @@ OZIMMU_API ozimmu_status_t ozimmu_dgemm_presliced_b(ozimmu_handle_t h, ozimmu_op
                                          const double *A, int64_t lda, const void *b_slices,
                                          const double *beta, double *C, int64_t ldc,
                                          int num_slices);
+
+/* ---- multi-GPU: C row blocks, B sliced once and broadcast ---------------
+ * BASELINE north_star: "C is partitioned into row blocks (2-D blocks for large n).  Each GPU
+ * slices its own A rows, B's slices are computed once and NCCL-broadcast over NVLink, and there
+ * are no other collectives."  One process (and one handle) per GPU.  Rank r passes its rows of
+ * op(A) (A_local, m_local rows, stored like A with leading dimension lda) and of C (C_local,
+ * ldc); op(B) (k x n) is read on `root` only (B may be NULL elsewhere).  The root slices op(B)
+ * in column chunks into a B-slice buffer (Alg. 4 on the columns of op(B)) and every chunk is
+ * broadcast to all ranks (s + 1 contiguous pieces: the chunk's rows of each INT8 plane and its
+ * int32 exponents) on the handle's collective stream; each rank's GEMM on a chunk waits only
+ * for that chunk, so later broadcasts overlap earlier GEMMs.  While broadcasts are in flight
+ * the fused GEMM leaves reserve_sms SMs free for the collective kernels (ozimmu_set_dist).
+ * C_local is bitwise what ozimmu_dgemm returns for those rows (no reduction exists; every
+ * element has the single-GPU operation sequence).  The 2-D partition is the same call on a
+ * communicator of {root} + one grid column, with that column block of op(B) as B (n = its
+ * width) and m_local = 0 on the root for the blocks it does not own.
+ * Every rank of the communicator must make the call, in the same order, with the same transB,
+ * n, k, ldb, alpha (= 0 or not), num_slices and ozimmu_set_dist settings.  num_slices = 0
+ * (INT8-AUTO) returns UNSUPPORTED: choosing s would need A's statistics from every rank.
+ * Asynchronous on the handle's stream like ozimmu_dgemm (the caller synchronises).
+ * Errors: as ozimmu_dgemm; OZIMMU_ERR_NCCL if libnccl cannot be loaded or a broadcast fails. */
+#define OZIMMU_NCCL_UNIQUE_ID_BYTES 128
+/* ncclGetUniqueId through the library's NCCL (root only; share the 128 bytes with the other
+ * ranks, e.g. through torch.distributed). */
+OZIMMU_API ozimmu_status_t ozimmu_nccl_get_unique_id(void *id_out);
+/* ncclCommInitRank(Config) on `device` (an ncclComm_t returned as void*).  max_ctas > 0 caps
+ * the CTAs of the communicator's kernels (ncclConfig_t.maxCTAs; pair it with reserve_sms). */
+OZIMMU_API ozimmu_status_t ozimmu_nccl_comm_init(void **comm_out, int nranks, const void *id,
+                                      int rank, int device, int max_ctas);
+OZIMMU_API ozimmu_status_t ozimmu_nccl_comm_destroy(void *comm);
+/* Multi-GPU settings of a handle: chunk_cols = columns per broadcast chunk (0: about n/8),
+ * reserve_sms = SMs the GEMM leaves to the collective while broadcasts are in flight (default
+ * 8), bcast_fp64 = 1 broadcasts FP64 op(B) (8 bytes per element instead of s) and slices each
+ * chunk on every rank (needs transB = N and ldb = k, else the INT8 planes are broadcast). */
+OZIMMU_API ozimmu_status_t ozimmu_set_dist(ozimmu_handle_t h, int chunk_cols, int reserve_sms,
+                                int bcast_fp64);
+/* comm: an ncclComm_t (e.g. from ozimmu_nccl_comm_init); rank and size are taken from it. */
+OZIMMU_API ozimmu_status_t ozimmu_dgemm_nccl(ozimmu_handle_t h, void *comm, int root,
+                                  ozimmu_op_t transA, ozimmu_op_t transB, int64_t m_local,
+                                  int64_t n, int64_t k, const double *alpha,
+                                  const double *A_local, int64_t lda, const double *B,
+                                  int64_t ldb, const double *beta, double *C_local, int64_t ldc,
+                                  int num_slices);
+/* The same driver over a caller-supplied broadcast: fn(ctx, buf, bytes, root, stream) must
+ * deliver `bytes` device bytes at buf from rank `root` to every rank, ordered after the work
+ * already enqueued on `stream` (a cudaStream_t as void*) and before work enqueued on it later
+ * (a synchronous implementation may synchronise the stream first); it returns 0 on success.
+ * Used by the tests to run the multi-rank logic over gloo. */
+typedef int (*ozimmu_bcast_fn)(void *ctx, void *buf, size_t bytes, int root, void *stream);
+OZIMMU_API ozimmu_status_t ozimmu_dgemm_bcast(ozimmu_handle_t h, ozimmu_bcast_fn fn, void *ctx,
+                                   int rank, int nranks, int root, ozimmu_op_t transA,
+                                   ozimmu_op_t transB, int64_t m_local, int64_t n, int64_t k,
+                                   const double *alpha, const double *A_local, int64_t lda,
+                                   const double *B, int64_t ldb, const double *beta,
+                                   double *C_local, int64_t ldc, int num_slices);
 
 /* ---- debug / parity exports (same kernels as the product path) -------------- */
 

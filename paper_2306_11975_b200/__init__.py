@@ -4,8 +4,8 @@ The product is the C-ABI library ``libozimmu.so`` (include/ozimmu.h) built from
 ``csrc/`` for sm_100a; this package is its thin Python binding plus the
 multi-GPU driver.  No CPU fallback exists.
 """
-from .ozimmu import (EXPORTS, Handle, OzimmuError, b_slices_bytes, lib, version,  # noqa: F401
-                     workspace_bytes)
+from .ozimmu import (BCAST_FN, EXPORTS, Handle, NcclComm, OzimmuError,  # noqa: F401
+                     b_slices_bytes, lib, nccl_unique_id, version, workspace_bytes)
 
-__all__ = ["Handle", "OzimmuError", "lib", "version", "workspace_bytes", "b_slices_bytes",
-           "EXPORTS"]
+__all__ = ["Handle", "NcclComm", "OzimmuError", "lib", "version", "workspace_bytes",
+           "b_slices_bytes", "nccl_unique_id", "BCAST_FN", "EXPORTS"]

@@ -425,6 +425,7 @@ const char *ozimmu_status_string(ozimmu_status_t s) {
     case OZIMMU_ERR_WORKSPACE: return "OZIMMU_ERR_WORKSPACE";
     case OZIMMU_ERR_CUDA: return "OZIMMU_ERR_CUDA";
     case OZIMMU_ERR_NOT_INITIALIZED: return "OZIMMU_ERR_NOT_INITIALIZED";
+    case OZIMMU_ERR_NCCL: return "OZIMMU_ERR_NCCL";
     }
     return "OZIMMU_UNKNOWN_STATUS";
 }
@@ -556,6 +557,14 @@ ozimmu_status_t ozimmu_destroy(ozimmu_handle_t h) {
     }
     if (h->h2d) cudaStreamDestroy(h->h2d);
     if (h->d2h) cudaStreamDestroy(h->d2h);
+    if (h->comm) {
+        cudaStreamSynchronize(h->comm);
+        cudaStreamDestroy(h->comm);
+    }
+    if (h->dist_buf) {
+        cudaDeviceSynchronize();
+        cudaFree(h->dist_buf);
+    }
     delete h;
     return OZIMMU_SUCCESS;
 }

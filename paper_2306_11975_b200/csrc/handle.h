@@ -40,6 +40,14 @@ struct ozimmu_ctx {
     // second stream for slicing op(B) concurrently with op(A) (fork / join by events)
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // multi-GPU (dist.cu): collective stream, settings (ozimmu_set_dist), the
+    // FP64 receive buffer of the FP64-broadcast variant
+    cudaStream_t comm = nullptr;
+    int dist_chunk_cols = 0;   // 0: about n/8 columns per broadcast chunk
+    int dist_reserve_sms = 8;  // SMs left to the collective while broadcasts are in flight
+    int dist_bcast_fp64 = 0;   // 1: broadcast FP64 B and slice it on every rank
+    void *dist_buf = nullptr;
+    size_t dist_buf_bytes = 0;
 };
 
 namespace ozimmu {

@@ -1,109 +1,29 @@
-"""Multi-GPU Ozaki DGEMM: C partitioned into row blocks, B sliced ONCE and its INT8
-planes broadcast to every rank (BASELINE north_star).
+"""Multi-GPU Ozaki DGEMM: thin orchestration over the library's multi-GPU driver (
+BASELINE north_star: C in row blocks, 2-D blocks for large n; every GPU slices its own A rows;
+B's slices are computed once and NCCL-broadcast over NVLink; no other collective).
 
-Rank r owns rows [r0, r1) of C and of op(A) and slices its own A rows (row
-exponents are per row -- no communication).  op(B) is sliced on the root only,
-chunk by chunk along n; each chunk's B-slice buffer (INT8 planes + int32 column
-exponents, ozimmu_b_slices_bytes) goes to all ranks with one NCCL broadcast over
-NVLink.  The GEMM on chunk c waits only for chunk c's broadcast, so the transfer
-of chunk c+1 overlaps the tensor-core work on chunk c (NCCL's stream vs the
-compute stream).  There is no reduction: every C element is computed on exactly
-one GPU by the same canonical operation sequence, so C is bitwise identical to the
-single-GPU result for every world size.
+The data path -- chunked slicing of op(B) on the root, the NCCL broadcasts on the handle's
+collective stream, the per-chunk GEMMs that wait only for their chunk, the SM reservation while
+broadcasts are in flight -- is inside libozimmu (csrc/dist.cu, ``ozimmu_dgemm_nccl``).  This
+module only decides who owns which rows / columns, creates the communicators (the NCCL unique
+id travels over torch.distributed, any backend), and makes the calls in a deadlock-free order.
 
-The math is done by a backend object (``CudaBackend`` wraps the C ABI); the
-orchestration here is plain torch.distributed and is unit-tested on CPU with
-gloo and a test-only backend.
+Engines (``engine.dgemm(root, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta,
+C_loc, ldc, s)``, one call per rank of the engine's group):
+  * ``NcclEngine``  -- the product: ozimmu_dgemm_nccl over an NCCL communicator.
+  * ``BcastEngine`` -- the same library driver over a host-staged torch.distributed broadcast
+    (ozimmu_dgemm_bcast): runs the multi-rank logic where NCCL cannot (several ranks on one
+    GPU, gloo); used by the tests.
+The CPU tests plug in an oracle-backed engine to check the partitioning logic here.
 """
+
 import torch
 import torch.distributed as dist
 
 
 def row_range(m, world, rank):
-    """Balanced contiguous row block [r0, r1) of rank `rank`."""
+    """Balanced contiguous block [r0, r1) of rank `rank` out of `world`."""
     return (m * rank) // world, (m * (rank + 1)) // world
-
-
-def col_chunks(n, chunk_cols):
-    chunk_cols = max(1, int(chunk_cols))
-    return [(c0, min(n, c0 + chunk_cols)) for c0 in range(0, n, chunk_cols)]
-
-
-class CudaBackend:
-    """Backend over libozimmu (device pointers, column-major, stream = current).
-
-    reserve_sms: SMs kept free of the fused GEMM while broadcasts are in flight.  The GEMM
-    is a persistent kernel with one ~227 KB-shared-memory CTA per SM, so an NCCL kernel
-    enqueued beside it only runs on SMs it leaves free; without a reserve the broadcast of
-    chunk c+1 would wait for the GEMM of chunk c instead of overlapping it.  Pair it with
-    NCCL_MAX_CTAS <= reserve_sms (bench.py does)."""
-
-    def __init__(self, handle, device, reserve_sms=0):
-        self.h = handle
-        self.device = torch.device("cuda", device) if isinstance(device, int) else device
-        self.reserve_sms = int(reserve_sms)
-
-    def overlap(self, on):
-        """GEMMs leave `reserve_sms` SMs free while `on` (broadcasts in flight)."""
-        if self.reserve_sms <= 0:
-            return
-        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-        self.h.set_max_sms(max(1, sms - self.reserve_sms) if on else 0)
-
-    def b_slices_bytes(self, n, k, s):
-        from .ozimmu import b_slices_bytes
-        return b_slices_bytes(n, k, s)
-
-    def alloc(self, nbytes):
-        return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-
-    def bind_stream(self):
-        self.h.set_stream(torch.cuda.current_stream(self.device))
-
-    def slice_b(self, transB, k, c0, c1, B, ldb, s, buf):
-        # column block [c0, c1) of op(B): N -> columns of B; T/C -> rows of B
-        off = c0 * ldb if transB == "N" else c0
-        self.h.slice_b(transB, k, c1 - c0, B.data_ptr() + 8 * off, ldb, s, buf)
-
-    def gemm(self, transA, m_loc, c0, c1, k, alpha, A_loc, lda, buf, beta, C_loc, ldc, s):
-        self.h.dgemm_presliced_b(transA, m_loc, c1 - c0, k, alpha, A_loc, lda, buf, beta,
-                                 C_loc.data_ptr() + 8 * c0 * ldc, ldc, s)
-
-
-def dgemm_rowblock(backend, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta,
-                   C_loc, ldc, s, root=0, chunk_cols=2048, group=None, bufs=None):
-    """C_loc = alpha op(A)[r0:r1] op(B) + beta C_loc on every rank.
-
-    A_loc: this rank's rows of op(A) (stored like A, m_loc rows), C_loc its rows of C.
-    B is only read on `root` (may be None elsewhere).  Returns the list of per-chunk
-    B-slice buffers (reusable via `bufs` to avoid re-allocation)."""
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    chunks = col_chunks(n, chunk_cols)
-    if bufs is None:
-        bufs = [backend.alloc(backend.b_slices_bytes(c1 - c0, k, s)) for c0, c1 in chunks]
-    works = []
-    # root: slice chunk c, then hand it to NCCL (which orders itself after the slicing
-    # on the current stream) while slicing chunk c+1
-    for (c0, c1), buf in zip(chunks, bufs):
-        if rank == root:
-            backend.slice_b(transB, k, c0, c1, B, ldb, s, buf)
-        if world > 1:
-            works.append(dist.broadcast(buf, src=root, group=group, async_op=True))
-        else:
-            works.append(None)
-    overlap = getattr(backend, "overlap", None)
-    last = len(chunks) - 1
-    for i, ((c0, c1), buf, w) in enumerate(zip(chunks, bufs, works)):
-        if w is not None:
-            w.wait()  # NCCL: the current stream waits for this chunk only
-        if overlap is not None and world > 1:
-            overlap(i < last)  # later chunks still in flight: leave SMs to NCCL
-        if m_loc > 0:
-            backend.gemm(transA, m_loc, c0, c1, k, alpha, A_loc, lda, buf, beta, C_loc, ldc, s)
-    if overlap is not None and world > 1:
-        overlap(False)
-    return bufs
 
 
 def grid_coords(rank, pr, pc):
@@ -111,64 +31,138 @@ def grid_coords(rank, pr, pc):
     return divmod(rank, pc)
 
 
-def make_grid_groups(pr, pc, root=0):
-    """Process groups for dgemm_grid2d: G_j = {root} + the ranks of grid column j.
-    Collective: every rank must call it (torch.distributed.new_group), in the same order."""
-    groups = []
-    for j in range(pc):
-        members = sorted({root} | {i * pc + j for i in range(pr)})
-        groups.append((members, dist.new_group(ranks=members)))
-    return groups
+def grid_members(pr, pc, root, j):
+    """Ranks of the broadcast group of grid column j: the root plus the ranks of column j."""
+    return sorted({root} | {i * pc + j for i in range(pr)})
 
 
-def dgemm_grid2d(backend, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta, C_loc,
-                 ldc, s, pr, pc, groups, root=0, chunk_cols=2048, bufs=None):
+# ---- engines ---------------------------------------------------------------------------
+
+def make_nccl_comm(device, group=None, max_ctas=0, members=None):
+    """An NCCL communicator over `group` (all ranks if None) created by libozimmu; the unique
+    id goes from the group's first member to the others over torch.distributed.  Collective
+    over the group.  max_ctas caps the communicator's CTAs (pair with the handle's
+    reserve_sms)."""
+    from .ozimmu import NcclComm, nccl_unique_id
+    if members is None:
+        members = list(range(dist.get_world_size()))
+    rank = dist.get_rank()
+    src = members[0]
+    obj = [nccl_unique_id() if rank == src else None]
+    if len(members) > 1:
+        dist.broadcast_object_list(obj, src=src, group=group)
+    return NcclComm(len(members), obj[0], members.index(rank), device, max_ctas)
+
+
+class NcclEngine:
+    """ozimmu_dgemm_nccl on `handle` over `comm` (an NcclComm); `root` is a rank of the comm."""
+
+    def __init__(self, handle, comm):
+        self.h, self.comm = handle, comm
+        self.launches = 0  # kernels the library launched for the last call
+
+    def dgemm(self, root, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta, C_loc,
+              ldc, s):
+        self.h.dgemm_nccl(self.comm, root, transA, transB, m_loc, n, k, alpha, A_loc, lda, B,
+                          ldb, beta, C_loc, ldc, s)
+        self.launches = self.h.report()["launches"]
+
+
+class BcastEngine:
+    """ozimmu_dgemm_bcast on `handle` with a synchronous host-staged broadcast over the
+    torch.distributed `group` (members: its global ranks in group order; `root` is an index
+    into them).  The callback synchronises the library's collective stream, copies the device
+    bytes to the host, broadcasts them and copies them back before returning, which satisfies
+    the ozimmu_bcast_fn ordering contract."""
+
+    def __init__(self, handle, group=None, members=None):
+        from .ozimmu import BCAST_FN
+        self.h, self.group = handle, group
+        self.members = members if members is not None else list(range(dist.get_world_size()))
+        self.me = self.members.index(dist.get_rank())
+        self.calls = 0
+        self.launches = 0  # kernels the library launched for the last call
+        self._fn = BCAST_FN(self._bcast)  # kept alive with the engine
+
+    def _bcast(self, ctx, buf, nbytes, root, stream):
+        try:
+            from cuda.bindings import runtime as rt
+            rt.cudaStreamSynchronize(stream)
+            host = torch.empty(int(nbytes), dtype=torch.uint8)
+            if self.me == root:
+                rt.cudaMemcpy(host.data_ptr(), buf, int(nbytes),
+                              rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
+            if len(self.members) > 1:
+                dist.broadcast(host, src=self.members[root], group=self.group)
+            if self.me != root:
+                rt.cudaMemcpy(buf, host.data_ptr(), int(nbytes),
+                              rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+            self.calls += 1
+            return 0
+        except Exception:  # reported to the library as a failed broadcast (OZIMMU_ERR_NCCL)
+            return 1
+
+    def dgemm(self, root, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta, C_loc,
+              ldc, s):
+        self.h.dgemm_bcast(self._fn, self.me, len(self.members), root, transA, transB, m_loc, n,
+                           k, alpha, A_loc, lda, B, ldb, beta, C_loc, ldc, s)
+        self.launches = self.h.report()["launches"]
+
+
+# ---- partitions ------------------------------------------------------------------------
+
+def dgemm_rowblock(engine, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta, C_loc,
+                   ldc, s, root=0):
+    """C_loc = alpha op(A)[r0:r1] op(B) + beta C_loc on every rank (row_range gives [r0, r1)).
+
+    A_loc: this rank's rows of op(A) (stored like A, m_loc rows); C_loc: its rows of C.  B is
+    only read on `root` (may be None elsewhere); ldb must be the same on every rank."""
+    engine.dgemm(root, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta, C_loc, ldc,
+                 s)
+
+
+def _col_block(transB, B, ldb, n0):
+    """Column n0 onwards of op(B): a device pointer (int) for torch tensors / ints, a view for
+    numpy arrays (the CPU test engine), None on non-root ranks."""
+    if B is None:
+        return None
+    if hasattr(B, "__array_interface__"):
+        return B[:, n0:] if transB == "N" else B[n0:, :]
+    base = B if isinstance(B, int) else B.data_ptr()
+    return base + 8 * (n0 * ldb if transB == "N" else n0)
+
+
+def dgemm_grid2d(engines, pr, pc, transA, transB, m_loc, n, k, alpha, A_loc, lda, B, ldb, beta,
+                 C_loc, ldc, s, root=0):
     """2-D partition of C ('large n'): rank (i, j) of a pr x pc grid owns rows
     row_range(m, pr, i) and columns row_range(n, pc, j) of C.  It slices its own rows of op(A)
-    (A row block i is replicated on the pc ranks of grid row i and sliced there, as the survey
-    proposes, so there is still no collective but the B one), and receives only the B-slice
-    buffers of its column block: the root slices op(B) chunk by chunk and broadcasts chunk c
-    of column block j inside group G_j = {root} + column j (make_grid_groups).  Every C element
-    is still computed on one GPU by the canonical operation sequence: C is bitwise equal to
-    the single-GPU result.  C_loc: this rank's m_loc x n_loc block (ldc); returns the buffers."""
+    (row block i is replicated on the pc ranks of grid row i, so the B broadcast stays the only
+    collective) and receives only the B slices of column block j, broadcast by the root inside
+    G_j = grid_members(pr, pc, root, j).  engines[j]: the engine of G_j on this rank (None if
+    the rank is not in G_j).  Every rank walks j = 0 .. pc-1 in the same order; the root takes
+    part in every G_j (m_loc = 0 where it owns no block).  C_loc: this rank's m_loc x n_loc
+    block (ldc)."""
     rank = dist.get_rank()
     i, j = grid_coords(rank, pr, pc)
-    plan = []  # (column block jj, c0, c1) in the order the root slices / broadcasts them
     for jj in range(pc):
-        n0, n1 = row_range(n, pc, jj)
-        for c0, c1 in col_chunks(n1 - n0, chunk_cols):
-            plan.append((jj, n0 + c0, n0 + c1))
-    mine = [(jj, c0, c1) for jj, c0, c1 in plan if jj == j]
-    if bufs is None:
-        bufs = {}
-    works = {}
-    for jj, c0, c1 in plan:
-        members, grp = groups[jj]
-        if rank not in members:
+        eng = engines[jj]
+        if eng is None:
             continue
-        key = (c0, c1)
-        if key not in bufs:
-            bufs[key] = backend.alloc(backend.b_slices_bytes(c1 - c0, k, s))
-        buf = bufs[key]
-        if rank == root:
-            backend.slice_b(transB, k, c0, c1, B, ldb, s, buf)
-        works[key] = dist.broadcast(buf, src=root, group=grp, async_op=True) \
-            if len(members) > 1 else None
-    n0, _ = row_range(n, pc, j)
-    overlap = getattr(backend, "overlap", None)
-    for q, (jj, c0, c1) in enumerate(mine):
-        w = works.get((c0, c1))
-        if w is not None:
-            w.wait()
-        if overlap is not None:
-            overlap(q < len(mine) - 1)
-        if m_loc > 0:
-            backend.gemm(transA, m_loc, c0 - n0, c1 - n0, k, alpha, A_loc, lda, bufs[(c0, c1)],
-                         beta, C_loc, ldc, s)
-    if overlap is not None:
-        overlap(False)
-    # the root may also have broadcast other columns' chunks: complete them before returning
-    for key, w in works.items():
-        if w is not None and not any((c0, c1) == key for _, c0, c1 in mine):
-            w.wait()
-    return bufs
+        n0, n1 = row_range(n, pc, jj)
+        mine = jj == j
+        members = grid_members(pr, pc, root, jj)
+        eng.dgemm(members.index(root), transA, transB, m_loc if mine else 0, n1 - n0, k, alpha,
+                  A_loc if mine else None, lda, _col_block(transB, B, ldb, n0) if rank == root
+                  else None, ldb, beta, C_loc if mine else None, ldc, s)
+
+
+def make_grid_engines(make_engine, pr, pc, root=0):
+    """engines[j] for dgemm_grid2d: make_engine(group, members) for every G_j this rank is in.
+    Collective: every rank must call it (torch.distributed.new_group), in the same order."""
+    rank = dist.get_rank()
+    out = []
+    for jj in range(pc):
+        members = grid_members(pr, pc, root, jj)
+        grp = dist.new_group(ranks=members)
+        out.append(make_engine(grp, members) if rank in members else None)
+    return out

@@ -18,7 +18,11 @@ LIB_PATH = os.environ.get("OZIMMU_LIB") or os.path.join(HERE, "libozimmu.so")
 
 OP = {"N": 0, "T": 1, "C": 2, 0: 0, 1: 1, 2: 2}
 STATUS = {0: "OZIMMU_SUCCESS", 1: "OZIMMU_ERR_INVALID_VALUE", 2: "OZIMMU_ERR_UNSUPPORTED",
-          3: "OZIMMU_ERR_WORKSPACE", 4: "OZIMMU_ERR_CUDA", 5: "OZIMMU_ERR_NOT_INITIALIZED"}
+          3: "OZIMMU_ERR_WORKSPACE", 4: "OZIMMU_ERR_CUDA", 5: "OZIMMU_ERR_NOT_INITIALIZED",
+          6: "OZIMMU_ERR_NCCL"}
+NCCL_UNIQUE_ID_BYTES = 128
+# int fn(void *ctx, void *buf, size_t bytes, int root, void *stream)  (ozimmu_bcast_fn)
+BCAST_FN = ct.CFUNCTYPE(ct.c_int, ct.c_void_p, ct.c_void_p, ct.c_size_t, ct.c_int, ct.c_void_p)
 EXP_NONFINITE = 0x7FFFFFFF
 
 # Every symbol include/ozimmu.h declares (checked by tests/test_abi.py).
@@ -30,7 +34,8 @@ EXPORTS = [
     "ozimmu_timing_enable", "ozimmu_timing_read", "ozimmu_zgemm", "ozimmu_zgemm_workspace_bytes",
     "ozimmu_set_auto", "ozimmu_auto_splits", "ozimmu_dgemm_strided_batched",
     "ozimmu_zgemm_strided_batched", "ozimmu_dgemm_host", "ozimmu_set_max_sms",
-    "ozimmu_set_auto_accuracy",
+    "ozimmu_set_auto_accuracy", "ozimmu_nccl_get_unique_id", "ozimmu_nccl_comm_init",
+    "ozimmu_nccl_comm_destroy", "ozimmu_set_dist", "ozimmu_dgemm_nccl", "ozimmu_dgemm_bcast",
 ]
 AUTO_LOSS, AUTO_ACCURACY = 1, 2
 AUTO_SMAX_DEFAULT = 18
@@ -101,6 +106,14 @@ def lib():
                                           i64, dp, vp, i64, i64, i64, i32], i32),
         "ozimmu_auto_splits": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, ct.POINTER(i32)], i32),
         "ozimmu_timing_read": ([H, ct.POINTER(Timing), i32], i32),
+        "ozimmu_nccl_get_unique_id": ([vp], i32),
+        "ozimmu_nccl_comm_init": ([ct.POINTER(vp), i32, vp, i32, i32, i32], i32),
+        "ozimmu_nccl_comm_destroy": ([vp], i32),
+        "ozimmu_set_dist": ([H, i32, i32, i32], i32),
+        "ozimmu_dgemm_nccl": ([H, vp, i32, i32, i32, i64, i64, i64, dp, vp, i64, vp, i64, dp, vp,
+                               i64, i32], i32),
+        "ozimmu_dgemm_bcast": ([H, BCAST_FN, vp, i32, i32, i32, i32, i32, i64, i64, i64, dp, vp,
+                                i64, vp, i64, dp, vp, i64, i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -148,6 +161,38 @@ def b_slices_bytes(n, k, num_slices):
 
 def version():
     return int(lib().ozimmu_version())
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId from the library's NCCL (call on one rank, share the bytes)."""
+    buf = ct.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    _check("ozimmu_nccl_get_unique_id", lib().ozimmu_nccl_get_unique_id(buf))
+    return bytes(buf.raw)
+
+
+class NcclComm:
+    """An NCCL communicator created through libozimmu (ozimmu_nccl_comm_init)."""
+
+    def __init__(self, nranks, uid, rank, device, max_ctas=0):
+        assert len(uid) == NCCL_UNIQUE_ID_BYTES
+        self.ptr = None
+        out = ct.c_void_p()
+        idbuf = ct.create_string_buffer(bytes(uid), NCCL_UNIQUE_ID_BYTES)
+        _check("ozimmu_nccl_comm_init", lib().ozimmu_nccl_comm_init(
+            ct.byref(out), int(nranks), idbuf, int(rank), int(device), int(max_ctas)))
+        self.ptr = out.value
+        self.rank, self.nranks = rank, nranks
+
+    def close(self):
+        if self.ptr:
+            lib().ozimmu_nccl_comm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Handle:
@@ -284,6 +329,27 @@ class Handle:
     def debug_pair(self, Ai, Bj, m, n, k, P_out):
         _check("ozimmu_debug_pair", lib().ozimmu_debug_pair(
             self._h, _ptr(Ai), _ptr(Bj), m, n, k, _ptr(P_out)))
+
+    # -- multi-GPU (include/ozimmu.h "multi-GPU") ----------------------------
+    def set_dist(self, chunk_cols=0, reserve_sms=8, bcast_fp64=False):
+        _check("ozimmu_set_dist", lib().ozimmu_set_dist(self._h, int(chunk_cols),
+                                                        int(reserve_sms), int(bool(bcast_fp64))))
+
+    def dgemm_nccl(self, comm, root, transA, transB, m_local, n, k, alpha, A_local, lda, B, ldb,
+                   beta, C_local, ldc, num_slices):
+        """C row blocks over an NCCL communicator (comm: NcclComm or raw ncclComm_t int)."""
+        raw = comm if isinstance(comm, int) else comm.ptr
+        _check("ozimmu_dgemm_nccl", lib().ozimmu_dgemm_nccl(
+            self._h, raw, int(root), OP[transA], OP[transB], m_local, n, k, _d(alpha),
+            _ptr(A_local), lda, _ptr(B), ldb, _d(beta), _ptr(C_local), ldc, int(num_slices)))
+
+    def dgemm_bcast(self, fn, rank, nranks, root, transA, transB, m_local, n, k, alpha, A_local,
+                    lda, B, ldb, beta, C_local, ldc, num_slices):
+        """The same driver over a caller broadcast fn (a BCAST_FN; keep it alive)."""
+        _check("ozimmu_dgemm_bcast", lib().ozimmu_dgemm_bcast(
+            self._h, fn, None, int(rank), int(nranks), int(root), OP[transA], OP[transB], m_local,
+            n, k, _d(alpha), _ptr(A_local), lda, _ptr(B), ldb, _d(beta), _ptr(C_local), ldc,
+            int(num_slices)))
 
     # -- torch convenience --------------------------------------------------------
     def matmul(self, A, B, num_slices, out=None):

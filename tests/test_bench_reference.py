@@ -31,3 +31,19 @@ def test_reference_arm_complex_workload_unavailable_line():
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and "unavailable" in line
+
+
+def test_multi_gpu_bench_refuses_without_enough_gpus():
+    """`bench.py --gpus 2` outside torchrun self-launches one rank per GPU; with fewer visible
+    GPUs than requested it must fail loudly rather than report a one-GPU number as N = 2."""
+    import torch
+    if torch.cuda.device_count() >= 2:
+        return
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env.pop("OZIMMU_BENCH_ONE_DEVICE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                       timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0
+    assert "refusing to report a multi-GPU number" in (r.stdout + r.stderr)

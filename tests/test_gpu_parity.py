@@ -395,26 +395,6 @@ def test_accuracy_gate_vs_dd(h, phi_idx, phi, s_eq):
     assert s_min is not None and abs(s_min - s_eq) <= 1, (s_min, st_cub)
 
 
-@pytest.mark.parametrize("ta,tb,chunk", [("N", "N", 100), ("T", "T", 64), ("N", "T", 1000)])
-def test_rowblock_driver_single_gpu_chunks(h, ta, tb, chunk):
-    """dist.dgemm_rowblock with the CUDA backend, world size 1 (no process group):
-    column-chunked B-slice buffers + presliced GEMMs == one ozimmu_dgemm, bitwise."""
-    torch = _torch()
-    from paper_2306_11975_b200 import dist as D
-    m, n, k, s = 300, 333, 500, 9
-    A = synth.gen_phi(*_stored(ta, m, k), 1.0, 1)
-    B = synth.gen_phi(*_stored(tb, k, n), 1.0, 2)
-    Cin = synth.gen_phi(m, n, 1.0, 3)
-    full = run_dgemm(h, ta, tb, m, n, k, 0.75, A, B, 1.25, Cin, s)
-    be = D.CudaBackend(h, 0)
-    dC = dev(Cin).view(n, m).t()  # column-major m x n view: C_loc.data_ptr() is C(0,0)
-    D.dgemm_rowblock(be, ta, tb, m, n, k, 0.75, dev(A), A.shape[0], dev(B), B.shape[0], 1.25,
-                     dC, m, s, chunk_cols=chunk)
-    torch.cuda.synchronize()
-    got = dC.t().contiguous().view(-1)
-    assert np.array_equal(host(got, m, n), full)
-
-
 @pytest.mark.parametrize("cap", [1, 2, 37, 100])
 def test_dgemm_capped_grid_bitwise(cap):
     """ozimmu_set_max_sms (persistent grid capped to `cap` SMs, CTA pairs rounded down) gives
