@@ -210,9 +210,10 @@ cudaError_t aux_join(ozimmu_handle_t h) {
 // mantissa loss is <= T for both operands.  ACCURACY (reading A18, Discussion P:713-734):
 // the smallest s <= s_max with eta(s) = sum_{t=0..s} rho_A(t) rho_B(s-t) <= tau u sqrt(k_acc),
 // u = 2^-53, summed in the order t = 0..s (the oracle's rule, oz_ref_auto_splits_acc).
-// s_max if none (*capped = true).
-int auto_decide(ozimmu_handle_t h, const unsigned long long *stat, int64_t k_acc, bool *capped) {
-    const int s_max = h->auto_smax;
+// Candidates s = 1..s_lim (the statistics hold t <= s_lim); s_lim if none (*capped = true).
+int auto_decide(ozimmu_handle_t h, const unsigned long long *stat, int64_t k_acc, int s_lim,
+                bool *capped) {
+    const int s_max = s_lim;
     *capped = false;
     if (h->auto_mode == OZIMMU_AUTO_LOSS) {
         for (int s = 1; s <= s_max; ++s) {
@@ -248,13 +249,20 @@ size_t auto_scratch_bytes(ozimmu_handle_t h, int64_t rows) {
     return r > keys ? r : keys;
 }
 cudaError_t auto_stats(ozimmu_handle_t h, const double *M, int64_t ld, bool contiguous,
-                       int64_t rows, int64_t kdim, int w, unsigned long long *stat_op,
+                       int64_t rows, int64_t kdim, int w, int s_lim, unsigned long long *stat_op,
                        void *scratch, cudaStream_t st, int *launches, int cpx) {
     if (h->auto_mode == OZIMMU_AUTO_LOSS)
-        return launch_mantissa_loss(M, ld, contiguous, rows, kdim, w, h->auto_smax, stat_op,
+        return launch_mantissa_loss(M, ld, contiguous, rows, kdim, w, s_lim, stat_op,
                                     static_cast<int32_t *>(scratch), h->num_sms, st, launches, cpx);
-    return launch_trunc_residual(M, ld, contiguous, rows, kdim, w, h->auto_smax, stat_op, scratch,
+    return launch_trunc_residual(M, ld, contiguous, rows, kdim, w, s_lim, stat_op, scratch,
                                  h->num_sms, st, launches, cpx);
+}
+
+// First-pass candidate limit: the accuracy rule's statistics cost grows with the number of t
+// they cover, and s <= 12 decides almost every input; a capped first pass is redone with
+// s_max (the statistics for t <= 12 are the same numbers, so the decision is unchanged).
+int auto_first_limit(ozimmu_handle_t h) {
+    return h->auto_mode == OZIMMU_AUTO_ACCURACY && h->auto_smax > 12 ? 12 : h->auto_smax;
 }
 
 // f2 INT8-AUTO: the statistics of both operands on the device, one D2H read (the call
@@ -272,23 +280,26 @@ ozimmu_status_t auto_select(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t t
     void *ws = nullptr;
     ozimmu_status_t st = get_ws(h, auto_scratch_bytes(h, m > n ? m : n), &ws);
     if (st) return st;
-    cudaError_t e =
-        cudaMemsetAsync(h->auto_dev, 0, 2 * kAutoNS * sizeof(unsigned long long), h->stream);
     const bool ac = transA != OZIMMU_OP_N, bc = transB == OZIMMU_OP_N;
-    // complex: contiguous vectors are 2k doubles (ld in doubles), strided ones k pairs
-    if (e == cudaSuccess)
-        e = auto_stats(h, A, cpx && ac ? 2 * lda : lda, ac, m, cpx && ac ? 2 * k : k, w,
-                       h->auto_dev, ws, h->stream, launches, cpx);
-    if (e == cudaSuccess)
-        e = auto_stats(h, B, cpx && bc ? 2 * ldb : ldb, bc, n, cpx && bc ? 2 * k : k, w,
-                       h->auto_dev + kAutoNS, ws, h->stream, launches, cpx);
-    unsigned long long host[2 * kAutoNS];
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(host, h->auto_dev, sizeof(host), cudaMemcpyDeviceToHost, h->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    if (e != cudaSuccess) return cuda_status(e);
     bool capped = false;
-    *s_out = auto_decide(h, host, k_acc, &capped);
+    for (int lim = auto_first_limit(h);; lim = h->auto_smax) {
+        cudaError_t e =
+            cudaMemsetAsync(h->auto_dev, 0, 2 * kAutoNS * sizeof(unsigned long long), h->stream);
+        // complex: contiguous vectors are 2k doubles (ld in doubles), strided ones k pairs
+        if (e == cudaSuccess)
+            e = auto_stats(h, A, cpx && ac ? 2 * lda : lda, ac, m, cpx && ac ? 2 * k : k, w, lim,
+                           h->auto_dev, ws, h->stream, launches, cpx);
+        if (e == cudaSuccess)
+            e = auto_stats(h, B, cpx && bc ? 2 * ldb : ldb, bc, n, cpx && bc ? 2 * k : k, w, lim,
+                           h->auto_dev + kAutoNS, ws, h->stream, launches, cpx);
+        unsigned long long host[2 * kAutoNS];
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(host, h->auto_dev, sizeof(host), cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) return cuda_status(e);
+        *s_out = auto_decide(h, host, k_acc, lim, &capped);
+        if (!capped || lim == h->auto_smax) break;
+    }
     h->auto_last_s = *s_out;
     h->auto_last_capped = capped;
     return OZIMMU_SUCCESS;

@@ -224,13 +224,14 @@ __global__ void __launch_bounds__(256) k_loss_strided(const double *__restrict__
 // then takes the smallest s with sum_{t=0..s} rho_A(t) rho_B(s-t) <= tau u sqrt(k)).
 // With |x| = M 2^e0 (M the integer significand, e0 its exponent), |x| 2^(wt-E) = M 2^-z,
 // z = E - e0 - wt fraction bits: the residual after t digits is the low z bits of M.
+template <int W, int SM>  // t = 1..SM (compile time); only t <= s_max are kept
 struct ResidAcc {
-    unsigned long long n[kMaxS + 1];  // [0] = D, [t] = N_t
+    unsigned long long n[SM + 1];  // [0] = D, [t] = N_t
     __device__ __forceinline__ void zero() {
 #pragma unroll
-        for (int t = 0; t <= kMaxS; ++t) n[t] = 0;
+        for (int t = 0; t <= SM; ++t) n[t] = 0;
     }
-    __device__ __forceinline__ void add(double x, int32_t E, int w, int s_max) {
+    __device__ __forceinline__ void add(double x, int32_t E) {
         const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
         const int be = static_cast<int>((u >> 52) & 0x7FF);
         const uint64_t fr = u & ((1ull << 52) - 1);
@@ -241,10 +242,39 @@ struct ResidAcc {
         // floor(M 2^(32 - z0)); for subnormal-only vectors z0 - 32 can be <= 0
         const int sh = z0 - 32;
         n[0] += sh <= 0 ? (M << (-sh)) : (sh >= 64 ? 0ull : (M >> sh));
+        if (z0 <= 96) {
+            // Fast path (every element within 43 bits of its vector's maximum): the fraction
+            // |x| / 2^E is exactly the 96-bit fixed-point V = M 2^(96 - z0) (limbs L0..L2).
+            // Digit t leaves the bits below position 96 - wt; the 32 just below the cut are
+            // the field at bit p = 64 - wt (one funnel shift, compile-time limbs), and the
+            // rounding-up bit is "V has a set bit below p", i.e. its lowest set bit < p.
+            const int v = 96 - z0;  // 0..95 (M < 2^53 and |x| < 2^E keep V < 2^96)
+            const uint64_t lo = v < 64 ? (M << v) : 0ull;
+            const uint64_t hi = v == 0 ? 0ull : (v < 64 ? (M >> (64 - v)) : (M << (v - 64)));
+            const uint32_t L[3] = {static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32),
+                                   static_cast<uint32_t>(hi)};
+            const int tzpos = __ffsll(static_cast<long long>(M)) - 1 + v;
 #pragma unroll
-        for (int t = 1; t <= kMaxS; ++t) {
-            if (t > s_max) break;
-            const int z = z0 - w * t;
+            for (int t = 1; t <= SM; ++t) {
+                const int p = 64 - W * t;
+                uint32_t f;
+                if (p >= 0) {
+                    const int li = p >> 5, bs = p & 31;
+                    const uint32_t hiw = li + 1 < 3 ? L[li + 1] : 0u;
+                    f = bs ? __funnelshift_r(L[li], hiw, bs) : L[li];
+                    n[t] += static_cast<unsigned long long>(f) + (tzpos < p ? 1ull : 0ull);
+                } else if (p > -32) {
+                    f = (L[0] & ((1u << (32 + p)) - 1u)) << (-p);
+                    n[t] += f;
+                }
+            }
+            return;
+        }
+        // general path: the residual after t digits is the low z bits of M, z = z0 - wt;
+        // ceil of its top 32 bits (z > 32: a shift plus a sticky bit)
+#pragma unroll
+        for (int t = 1; t <= SM; ++t) {
+            const int z = z0 - W * t;
             uint64_t f;
             if (z <= 0) {
                 f = 0;
@@ -253,10 +283,10 @@ struct ResidAcc {
                 if (z <= 32) {
                     f = R << (32 - z);
                 } else {
-                    const int d = z - 32;  // ceil(R / 2^d): shift plus a sticky bit
-                    const uint64_t hi = d >= 64 ? 0ull : (R >> d);
-                    const uint64_t lo = d >= 64 ? R : (R & ((1ull << d) - 1));
-                    f = hi + (lo != 0 ? 1ull : 0ull);
+                    const int d = z - 32;
+                    const uint64_t hi2 = d >= 64 ? 0ull : (R >> d);
+                    const uint64_t lo2 = d >= 64 ? R : (R & ((1ull << d) - 1));
+                    f = hi2 + (lo2 != 0 ? 1ull : 0ull);
                 }
             }
             n[t] += f;
@@ -266,12 +296,13 @@ struct ResidAcc {
 
 // Contiguous vectors: persistent 256-thread blocks, one vector at a time (pass 1 exponent,
 // pass 2 the sums, block-reduced and written to sums[r][0..s_max]).
+template <int W, int SM>
 __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__ M, int64_t ld,
-                                                      int64_t rows, int64_t kdim, int w, int s_max,
+                                                      int64_t rows, int64_t kdim, int s_max,
                                                       unsigned long long *__restrict__ sums,
                                                       int32_t *__restrict__ keys_out) {
     __shared__ int32_t kred[8];
-    __shared__ unsigned long long red[8][kMaxS + 1];
+    __shared__ unsigned long long red[8][SM + 1];
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const double *v = M + r * ld;
         int32_t key = kKeyEmpty;
@@ -294,7 +325,7 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
         __syncthreads();  // kred is rewritten for the next vector
         if (threadIdx.x == 0) keys_out[r] = key;
         if (key == kExpNonFinite || key == kKeyEmpty) continue;  // skipped vector
-        ResidAcc acc;
+        ResidAcc<W, SM> acc;
         acc.zero();
         l = threadIdx.x;
         for (; l + 3 * 256 < kdim; l += 4 * 256) {
@@ -302,12 +333,11 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
 #pragma unroll
             for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc.add(x[i], key, w, s_max);
+            for (int i = 0; i < 4; ++i) acc.add(x[i], key);
         }
-        for (; l < kdim; l += 256) acc.add(__ldg(v + l), key, w, s_max);
+        for (; l < kdim; l += 256) acc.add(__ldg(v + l), key);
 #pragma unroll
-        for (int t = 0; t <= kMaxS; ++t) {
-            if (t > s_max) break;
+        for (int t = 0; t <= SM; ++t) {
             unsigned long long x = acc.n[t];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffff, x, o);
@@ -327,16 +357,16 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
 // Strided vectors (element l of vector r at M[r + l ld]; complex: the (re, im) pair): one
 // thread per vector and a slice of l per blockIdx.y, partial sums added to sums[r][.]
 // (zeroed by the caller; integer atomics, so the totals do not depend on the order).
-template <int CPX>
+template <int W, int SM, int CPX>
 __global__ void __launch_bounds__(256) k_resid_strided(const double *__restrict__ M, int64_t ld,
                                                        int64_t rows, int64_t kdim, int64_t lchunk,
-                                                       const int32_t *__restrict__ keys, int w,
+                                                       const int32_t *__restrict__ keys,
                                                        int s_max,
                                                        unsigned long long *__restrict__ sums) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
     const int32_t key = r < rows ? keys[r] : kKeyEmpty;
     if (key == kExpNonFinite || key == kKeyEmpty) return;
-    ResidAcc acc;
+    ResidAcc<W, SM> acc;
     acc.zero();
     const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
     const int64_t l1 = min(kdim, l0 + lchunk);
@@ -344,8 +374,8 @@ __global__ void __launch_bounds__(256) k_resid_strided(const double *__restrict_
         const double2 *Mc = reinterpret_cast<const double2 *>(M);
         for (int64_t l = l0; l < l1; ++l) {
             const double2 z = __ldg(Mc + r + l * ld);
-            acc.add(z.x, key, w, s_max);
-            acc.add(z.y, key, w, s_max);
+            acc.add(z.x, key);
+            acc.add(z.y, key);
         }
     } else {
         int64_t l = l0;
@@ -354,12 +384,12 @@ __global__ void __launch_bounds__(256) k_resid_strided(const double *__restrict_
 #pragma unroll
             for (int i = 0; i < 4; ++i) x[i] = __ldg(M + r + (l + i) * ld);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc.add(x[i], key, w, s_max);
+            for (int i = 0; i < 4; ++i) acc.add(x[i], key);
         }
-        for (; l < l1; ++l) acc.add(__ldg(M + r + l * ld), key, w, s_max);
+        for (; l < l1; ++l) acc.add(__ldg(M + r + l * ld), key);
     }
 #pragma unroll
-    for (int t = 0; t <= kMaxS; ++t) {
+    for (int t = 0; t <= SM; ++t) {
         if (t > s_max) break;
         if (acc.n[t]) atomicAdd(&sums[r * (s_max + 1) + t], acc.n[t]);
     }
@@ -387,40 +417,69 @@ __global__ void k_resid_rho(const unsigned long long *__restrict__ sums, const i
 // Accuracy-targeted AUTO statistics of the vectors of op(M): rho_out (device, s_max + 1 uint64
 // holding doubles; max-accumulated, caller zeroes it).  scratch: device uint64
 // [rows (s_max + 1)] + int32 [rows] keys.
+namespace {
+template <int W, int SM>
+cudaError_t resid_sums(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
+                       int s_max, unsigned long long *sums, int32_t *keys, int num_sms,
+                       cudaStream_t st, int *launches, int cpx) {
+    if (contiguous) {
+        int64_t blocks = 4 * (int64_t)num_sms;
+        if (blocks > rows) blocks = rows;
+        k_resid_contig<W, SM><<<(unsigned)blocks, 256, 0, st>>>(M, ld, rows, kdim, s_max, sums, keys);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * rows * (s_max + 1), st);
+    if (e != cudaSuccess) return e;
+    e = launch_expscan(M, ld, rows, kdim, keys, num_sms, st, launches, cpx);
+    if (e != cudaSuccess) return e;
+    const int64_t rblocks = ceil_div(rows, 256);
+    int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
+    if (ysplit < 1) ysplit = 1;
+    int64_t lchunk = ceil_div(kdim, ysplit);
+    if (lchunk < 256) lchunk = 256;
+    ysplit = ceil_div(kdim, lchunk);
+    if (cpx)
+        k_resid_strided<W, SM, 1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+            M, ld, rows, kdim, lchunk, keys, s_max, sums);
+    else
+        k_resid_strided<W, SM, 0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
+            M, ld, rows, kdim, lchunk, keys, s_max, sums);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t resid_sums_w(const double *M, int64_t ld, bool contiguous, int64_t rows, int64_t kdim,
+                         int s_max, unsigned long long *sums, int32_t *keys, int num_sms,
+                         cudaStream_t st, int *launches, int cpx) {
+    // t = 1..12 covers every decision up to s = 12 (the usual case); larger s_max take the
+    // full-width instance
+    if (s_max <= 12)
+        return resid_sums<W, 12>(M, ld, contiguous, rows, kdim, s_max, sums, keys, num_sms, st,
+                                 launches, cpx);
+    return resid_sums<W, kMaxS>(M, ld, contiguous, rows, kdim, s_max, sums, keys, num_sms, st,
+                                launches, cpx);
+}
+}  // namespace
+
+// Accuracy-targeted AUTO statistics of the vectors of op(M): rho_out (device, s_max + 1 uint64
+// holding doubles; max-accumulated, caller zeroes it).  scratch: device uint64
+// [rows (s_max + 1)] + int32 [rows] keys.
 cudaError_t launch_trunc_residual(const double *M, int64_t ld, bool contiguous, int64_t rows,
                                   int64_t kdim, int w, int s_max, unsigned long long *rho_out,
                                   void *scratch, int num_sms, cudaStream_t st, int *launches,
                                   int cpx) {
     if (rows <= 0 || kdim <= 0) return cudaSuccess;
-    if (s_max < 1 || s_max > kMaxS || w < 1 || w > 7) return cudaErrorInvalidValue;
+    if (s_max < 1 || s_max > kMaxS || w < 5 || w > 7) return cudaErrorInvalidValue;
     unsigned long long *sums = static_cast<unsigned long long *>(scratch);
     int32_t *keys = reinterpret_cast<int32_t *>(sums + rows * (s_max + 1));
     cudaError_t e;
-    if (contiguous) {
-        int64_t blocks = 4 * (int64_t)num_sms;
-        if (blocks > rows) blocks = rows;
-        k_resid_contig<<<(unsigned)blocks, 256, 0, st>>>(M, ld, rows, kdim, w, s_max, sums, keys);
-        ++*launches;
-    } else {
-        e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * rows * (s_max + 1), st);
-        if (e != cudaSuccess) return e;
-        e = launch_expscan(M, ld, rows, kdim, keys, num_sms, st, launches, cpx);
-        if (e != cudaSuccess) return e;
-        const int64_t rblocks = ceil_div(rows, 256);
-        int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
-        if (ysplit < 1) ysplit = 1;
-        int64_t lchunk = ceil_div(kdim, ysplit);
-        if (lchunk < 256) lchunk = 256;
-        ysplit = ceil_div(kdim, lchunk);
-        if (cpx)
-            k_resid_strided<1><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-                M, ld, rows, kdim, lchunk, keys, w, s_max, sums);
-        else
-            k_resid_strided<0><<<dim3((unsigned)rblocks, (unsigned)ysplit), 256, 0, st>>>(
-                M, ld, rows, kdim, lchunk, keys, w, s_max, sums);
-        ++*launches;
+    switch (w) {
+    case 7: e = resid_sums_w<7>(M, ld, contiguous, rows, kdim, s_max, sums, keys, num_sms, st, launches, cpx); break;
+    case 6: e = resid_sums_w<6>(M, ld, contiguous, rows, kdim, s_max, sums, keys, num_sms, st, launches, cpx); break;
+    default: e = resid_sums_w<5>(M, ld, contiguous, rows, kdim, s_max, sums, keys, num_sms, st, launches, cpx); break;
     }
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int ty = 256 / 64;  // 64 threads (t = 0..s_max) x 4 vectors per block
     k_resid_rho<<<(unsigned)ceil_div(rows, ty), dim3(64, ty), 0, st>>>(sums, keys, rows, w, s_max,

@@ -111,11 +111,13 @@ cudaError_t aux_fork(ozimmu_handle_t h);
 cudaError_t aux_join(ozimmu_handle_t h);
 // INT8-AUTO (f2): statistics slots, decision, scratch, statistics kernels, selection.
 constexpr int kAutoNS = 33;
-int auto_decide(ozimmu_handle_t h, const unsigned long long *stat, int64_t k_acc, bool *capped);
+int auto_decide(ozimmu_handle_t h, const unsigned long long *stat, int64_t k_acc, int s_lim,
+                bool *capped);
 size_t auto_scratch_bytes(ozimmu_handle_t h, int64_t rows);
 cudaError_t auto_stats(ozimmu_handle_t h, const double *M, int64_t ld, bool contiguous,
-                       int64_t rows, int64_t kdim, int w, unsigned long long *stat_op,
+                       int64_t rows, int64_t kdim, int w, int s_lim, unsigned long long *stat_op,
                        void *scratch, cudaStream_t st, int *launches, int cpx);
+int auto_first_limit(ozimmu_handle_t h);
 ozimmu_status_t auto_select(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t transB, int64_t m,
                             int64_t n, int64_t k, const double *A, int64_t lda, const double *B,
                             int64_t ldb, int *s_out, int *launches, bool cpx = false);

@@ -214,6 +214,7 @@ ozimmu_status_t host_auto(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t tra
     int launches = 0;
     void *bbuf = nullptr;
     int s = s_max;
+    const int lim1 = auto_first_limit(h);
 #define OZ_TRY(x) do { if (e == cudaSuccess) e = (x); } while (0)
     OZ_TRY(cudaEventRecord(ev_start, cs));
     OZ_TRY(cudaStreamWaitEvent(h->h2d, ev_start, 0));
@@ -229,8 +230,8 @@ ozimmu_status_t host_auto(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t tra
             OZ_TRY(copy2d(dA + r0, m, A + r0, lda, mi, k, cudaMemcpyHostToDevice, h->h2d));
         OZ_TRY(cudaEventRecord(ev_in[i], h->h2d));
         OZ_TRY(cudaStreamWaitEvent(cs, ev_in[i], 0));
-        OZ_TRY(auto_stats(h, src, a_contig ? k : m, a_contig, mi, k, w, h->auto_dev, keys, cs,
-                          &launches, 0));
+        OZ_TRY(auto_stats(h, src, a_contig ? k : m, a_contig, mi, k, w, lim1, h->auto_dev, keys,
+                          cs, &launches, 0));
     }
     for (int64_t j = 0; j < J; ++j) {
         const int64_t c0 = j * nbk, nc = (j == J - 1) ? n - c0 : nbk;
@@ -241,8 +242,8 @@ ozimmu_status_t host_auto(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t tra
             OZ_TRY(copy2d(dB + c0, n, B + c0, ldb, nc, k, cudaMemcpyHostToDevice, h->h2d));
         OZ_TRY(cudaEventRecord(ev_in[P + j], h->h2d));
         OZ_TRY(cudaStreamWaitEvent(cs, ev_in[P + j], 0));
-        OZ_TRY(auto_stats(h, src, b_contig ? k : n, b_contig, nc, k, w, h->auto_dev + NS, keys,
-                          cs, &launches, 0));
+        OZ_TRY(auto_stats(h, src, b_contig ? k : n, b_contig, nc, k, w, lim1, h->auto_dev + NS,
+                          keys, cs, &launches, 0));
     }
     if (*beta != 0.0) OZ_TRY(copy2d(dC, m, C, ldc, m, n, cudaMemcpyHostToDevice, h->h2d));
     // ---- choose s (one D2H read) ----
@@ -250,9 +251,20 @@ ozimmu_status_t host_auto(ozimmu_handle_t h, ozimmu_op_t transA, ozimmu_op_t tra
     OZ_TRY(cudaMemcpyAsync(sums, h->auto_dev, sizeof(sums), cudaMemcpyDeviceToHost, cs));
     OZ_TRY(cudaStreamSynchronize(cs));
     OZ_TRY(cudaStreamSynchronize(h->h2d));  // C (beta != 0) is on the device too
+    bool capped = false;
+    if (e == cudaSuccess) s = auto_decide(h, sums, k, lim1, &capped);
+    if (e == cudaSuccess && capped && lim1 < s_max) {
+        // second pass over the whole (landed) operands with every candidate s
+        OZ_TRY(cudaMemsetAsync(h->auto_dev, 0, 2 * NS * sizeof(unsigned long long), cs));
+        OZ_TRY(auto_stats(h, dA, a_contig ? k : m, a_contig, m, k, w, s_max, h->auto_dev, keys,
+                          cs, &launches, 0));
+        OZ_TRY(auto_stats(h, dB, b_contig ? k : n, b_contig, n, k, w, s_max, h->auto_dev + NS,
+                          keys, cs, &launches, 0));
+        OZ_TRY(cudaMemcpyAsync(sums, h->auto_dev, sizeof(sums), cudaMemcpyDeviceToHost, cs));
+        OZ_TRY(cudaStreamSynchronize(cs));
+        if (e == cudaSuccess) s = auto_decide(h, sums, k, s_max, &capped);
+    }
     if (e == cudaSuccess) {
-        bool capped = false;
-        s = auto_decide(h, sums, k, &capped);
         h->auto_last_capped = capped;
         h->auto_last_s = s;
         const size_t need = ozimmu_b_slices_bytes(n, k, s);
