@@ -89,7 +89,7 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     for (auto &sh : shapes) {
         GemmPlan gp;
         if (!plan_gemm(s, w, sh[0], sh[1], k_pad, gemm_sms(h), &gp)) return false;
-        const size_t c = chunk_scratch_bytes(gp, s);
+        const size_t c = chunk_scratch_bound(gp, s, h->num_sms);  // any region shape
         if (c > scratch) scratch = c;
     }
     size_t off = 0;

@@ -51,13 +51,40 @@ OZ_EXTERN32(7) OZ_EXTERN32(8) OZ_EXTERN32(9) OZ_EXTERN32(10)
 #undef OZ_EXTERN32
 }  // namespace gemm_detail
 
+// INT32 budget of one accumulator region over the whole K: no K chunks needed
+// when a level's pairs fit one region, or two regions of G pairs (T = 2) fit TMEM.
+static bool budget_one_chunk(int s, int w, int64_t k_pad, int nc) {
+    const int64_t d = ((int64_t)1 << w) - 1;
+    const int64_t kfull = ceil_div(k_pad, kKB) * kKB;
+    const int64_t G = (int64_t)2147483647 / (kfull * d * d);
+    if (G >= s) return true;
+    return G >= 1 && (s + G - 1) / G == 2 && ((int64_t)s + (s - G)) * nc <= 512;
+}
+
 bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, GemmPlan *p) {
     if (s < 1 || s > 32 || w < 1) return false;
     int nc = nc_for(s);
-    // Small problems: with few tiles the last, partial wave dominates; N_c = 32 gives 1.5-2x
-    // the tiles (an instance exists for s <= 10) at ~4 % lower MMA-mix efficiency.  Measured
-    // crossover: better up to ~5 waves of default tiles (1024^3 GEMM 67 -> 47 us).
-    if (nc > 32 && s <= 10 &&
+    // Stream-K (OZIMMU_SK: 0 off = default, 1 forced, -1 auto): when the tiles of a problem fill
+    // only a few waves and the last one is partial, clusters share the K loop of the tail
+    // units instead (k_oz_gemm); then the default tile width keeps its better MMA mix.  Needs
+    // one INT32-safe pass over K (no K chunks).  Off by default: measured slower than the
+    // data-parallel schedule at 1024^3-2048^3 (53 -> 90 us and 261 -> 313 us GEMM), the
+    // fixup's L2 round trips for a split unit's int32 partials (s N_c values per row) cost
+    // more than the partial wave they remove.  Bit-identical either way.
+    static const int sk_env = getenv("OZIMMU_SK") ? atoi(getenv("OZIMMU_SK")) : 0;
+    bool sk = false;
+    if (sk_env != 0 && budget_one_chunk(s, w, k_pad, nc)) {
+        const int64_t units = ceil_div(m, kBlockM) * ceil_div(ceil_div(n, (int64_t)nc), 2);
+        const int64_t G = num_sms / 2 > 0 ? num_sms / 2 : 1;  // CTA pairs
+        const int64_t waves = ceil_div(units, G);
+        // partial last wave costing > 2 % of a data-parallel schedule of <= 8 waves
+        sk = sk_env == 1 || (waves <= 8 && (waves * G - units) * 50 > waves * G);
+    }
+    // Small problems without stream-K: with few tiles the last, partial wave dominates; N_c =
+    // 32 gives 1.5-2x the tiles (an instance exists for s <= 10) at ~4 % lower MMA-mix
+    // efficiency.  Measured crossover: better up to ~5 waves of default tiles (1024^3 GEMM
+    // 67 -> 47 us).
+    if (!sk && nc > 32 && s <= 10 &&
         ceil_div(m, kBlockM) * ceil_div(n, (int64_t)nc) <= 5 * (int64_t)num_sms)
         nc = 32;
     const size_t smem_budget = 232448 - 3072;  // 227 KB opt-in max minus barriers/align/static
@@ -106,6 +133,17 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     const int64_t tiles = ceil_div(m, kBlockM) * ceil_div(n, nc);
     p->grid = (int)(tiles < num_sms ? tiles : num_sms);
     if (p->grid < 1) p->grid = 1;
+    // stream-K counter slots: units x cluster size <= (tiles_m + 1) x (tiles_n + 1)
+    p->tiles = (ceil_div(m, kBlockM) + 1) * (ceil_div(n, nc) + 1);
+    p->sk = sk && p->k_chunks == 1 ? 1 : 0;
+    if (p->sk) {
+        // every cluster takes a share of the K loops, but a unit is cut into at most ~4 parts
+        // (fewer for short K: each part's partial sums cost a write and a read in the fixup)
+        int64_t parts = p->num_k_blocks / 4;
+        parts = parts < 1 ? 1 : (parts > 4 ? 4 : parts);
+        const int64_t g = tiles * parts;
+        p->grid = (int)(g < num_sms ? g : num_sms);
+    }
     p->smem_bytes = 1024 /*align slack*/ + b_stage * b_stages + a_stage * a_stages +
                     8 * (2 * b_stages + 2 * a_stages + 2) + 16;
     int cols = 32;
@@ -115,7 +153,16 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     return true;
 }
 
+// Stream-K scratch: arrival counters [units x cl <= tiles + 4] then int32 partial level sums
+// [grid CTAs][2 slots][used TMEM columns <= 512][128 rows].
+static size_t sk_scratch(int64_t tiles, int grid) {
+    const size_t cnt = ((size_t)(tiles + 4) * sizeof(int) + 255) / 256 * 256;
+    return cnt + (size_t)grid * 2 * 512 * kBlockM * sizeof(int32_t);
+}
+size_t sk_counters_bytes(int64_t tiles) { return ((size_t)(tiles + 4) * sizeof(int) + 255) / 256 * 256; }
+
 size_t chunk_scratch_bytes(const GemmPlan &p, int s) {
+    if (p.sk) return sk_scratch(p.tiles, p.grid);
     if (p.k_chunks <= 1) return 0;
     return (size_t)p.grid * s * p.tile_n * kBlockM * sizeof(int64_t);
 }
@@ -124,10 +171,13 @@ size_t chunk_scratch_bytes(const GemmPlan &p, int s) {
 // max_sms SMs: the tile width may switch between 32 and nc_for(s) with the cap (small-problem
 // rule in plan_gemm), and the grid is at most max_sms CTAs.
 size_t chunk_scratch_bound(const GemmPlan &p, int s, int max_sms) {
-    if (p.k_chunks <= 1) return 0;
-    const int nc = nc_for(s) > p.tile_n ? nc_for(s) : p.tile_n;
     const int g = p.grid > max_sms ? p.grid : max_sms;
-    return (size_t)g * s * nc * kBlockM * sizeof(int64_t);
+    // stream-K may be chosen under any SM cap / for any sub-shape with one pass over K; its
+    // counters are bounded by the tiles of the narrowest tile width
+    const size_t skb = sk_scratch(p.tiles * (p.tile_n / 16 > 0 ? p.tile_n / 16 : 1), g);
+    const int nc = nc_for(s) > p.tile_n ? nc_for(s) : p.tile_n;
+    const size_t kcb = (size_t)g * s * nc * kBlockM * sizeof(int64_t);
+    return skb > kcb ? skb : kcb;
 }
 
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st,

@@ -48,6 +48,69 @@ struct KParams {
     int G;                       // pairs per INT32 accumulator (sub-group size)
     int T;                       // accumulator regions (sub-groups) per level, 1 or 2
     uint32_t region_col[2];      // TMEM column of region t (region t holds levels j < s - tG)
+    // stream-K schedule (small problems, k_chunks == 1): cluster c of the G clusters takes the
+    // kb-units [c W / G, (c+1) W / G) of W = num_units x num_k_blocks, so the last partial wave
+    // disappears; a unit split between clusters leaves exact int32 partial level sums in
+    // sk_part and the last cluster to finish it (sk_count) adds them and runs the epilogue.
+    int sk;
+    int64_t sk_total;            // W
+    int *sk_count;               // [num_units][cl] arrivals (zeroed before the launch)
+    int32_t *sk_part;            // [G][2 slots][cl][used_cols][128] partial level sums
+    uint32_t used_cols;          // TMEM columns holding level sums
+};
+
+// ---- work schedule -------------------------------------------------------------------------
+// Data-parallel: units u = c, c + G, .. (G = clusters in the grid), every unit over the whole
+// K.  Stream-K: the contiguous kb-range of cluster c, cut into segments at unit boundaries;
+// only a cluster's first and last segment can be a partial unit (slots 0 and 1).
+__device__ __forceinline__ int64_t sk_begin(const KParams &P, int64_t c, int64_t G) {
+    return c * P.sk_total / G;
+}
+// the cluster whose kb-range holds kb-unit g
+__device__ __forceinline__ int64_t sk_owner(const KParams &P, int64_t g, int64_t G) {
+    int64_t c = g * G / P.sk_total;
+    while (c + 1 < G && sk_begin(P, c + 1, G) <= g) ++c;
+    while (c > 0 && sk_begin(P, c, G) > g) --c;
+    return c;
+}
+struct WorkIter {
+    int64_t u, kb0, kb1;  // current unit and its k-block range
+    bool first;           // first segment of this cluster (stream-K partial slot 0)
+    int64_t g, ge;        // stream-K cursor / end (kb-units)
+    __device__ __forceinline__ void start(const KParams &P) {
+        const int64_t G = gridDim.x / P.cl, c = blockIdx.x / P.cl;
+        first = true;
+        if (P.sk) {
+            g = sk_begin(P, c, G);
+            ge = sk_begin(P, c + 1, G);
+            seg(P);
+        } else {
+            u = c;
+            kb0 = 0;
+            kb1 = P.num_k_blocks;
+        }
+    }
+    __device__ __forceinline__ void seg(const KParams &P) {
+        u = g / P.num_k_blocks;
+        kb0 = g - u * P.num_k_blocks;
+        kb1 = kb0 + (ge - g);
+        if (kb1 > P.num_k_blocks) kb1 = P.num_k_blocks;
+    }
+    __device__ __forceinline__ bool valid(const KParams &P) const {
+        return P.sk ? g < ge : u < P.num_units;
+    }
+    __device__ __forceinline__ bool full(const KParams &P) const {
+        return kb0 == 0 && kb1 == P.num_k_blocks;
+    }
+    __device__ __forceinline__ void next(const KParams &P) {
+        first = false;
+        if (P.sk) {
+            g += kb1 - kb0;
+            if (g < ge) seg(P);
+        } else {
+            u += gridDim.x / P.cl;
+        }
+    }
 };
 
 // N_c (output columns per tile) as a function of s: the largest of {64, 48, 32, 16} with
@@ -228,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const KParams P) {
     constexpr int NC = NCV;  // output columns per tile (nc_for(S), or 32 for small problems)
     __shared__ int32_t eb_s[2][64];  // column exponents of the current tile (double-buffered)
+    __shared__ int sk_old;           // stream-K: arrivals before this CTA's part of a unit
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>(
@@ -291,18 +355,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t wave = 0, bidx = 0;  // tile wave, soft-barrier instance
             long long st_w = 0, st_pa = 0, st_pb = 0;
             const uint32_t b_tx = (uint32_t)(s * NC * kKB), a_tx = (uint32_t)(kBlockM * kKB);
-            for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl, ++wave) {
+            WorkIter it;
+            for (it.start(P); it.valid(P); it.next(P), ++wave) {
                 int64_t mb, nb;
-                tile_coords(u, P, rank, mb, nb);
+                tile_coords(it.u, P, rank, mb, nb);
                 long long c0 = P.stats ? clock64() : 0;
                 wave_sync(P, wave, bidx++);
                 if (P.stats) st_w += clock64() - c0;
                 // K snake: odd waves walk K backwards, so a wave starts on the k-blocks the
                 // previous wave (same A row blocks) touched last, still in L2.  The INT32
                 // sums are order-independent; K chunks (int64 partials) keep the forward order.
-                const bool rev = OZ_KSNAKE && P.k_chunks == 1 && (wave & 1);
+                const bool rev = OZ_KSNAKE && !P.sk && P.k_chunks == 1 && (wave & 1);
                 auto kmap = [&](int64_t kb) { return rev ? P.num_k_blocks - 1 - kb : kb; };
-                for (int64_t kb = 0; kb < P.num_k_blocks; ++kb) {
+                for (int64_t kb = it.kb0; kb < it.kb1; ++kb) {
                     const int64_t kx = kmap(kb);
                     if (P.ksync && kb > 0 && kb % P.ksync == 0) {
                         long long c3 = P.stats ? clock64() : 0;
@@ -409,11 +474,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
 
-        for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl) {
+        WorkIter it;
+        for (it.start(P); it.valid(P); it.next(P)) {
             for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
-                const int64_t kb0 = (int64_t)c * P.chunk_blocks;
+                int64_t kb0 = (int64_t)c * P.chunk_blocks;
                 int64_t kb1 = kb0 + P.chunk_blocks;
                 kb1 = kb1 < P.num_k_blocks ? kb1 : P.num_k_blocks;
+                if (P.sk) {  // stream-K (k_chunks == 1): this cluster's k-blocks of the unit
+                    kb0 = it.kb0;
+                    kb1 = it.kb1;
+                }
                 // the epilogue has read and zeroed the accumulator (phase acc_iter)
                 {
                     long long c0 = P.stats ? clock64() : 0;
@@ -504,7 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         uint32_t acc_iter = 0, tile_iter = 0;
         long long st_e = 0, st_et = 0, st_es = 0;
-        for (int64_t u = blockIdx.x / P.cl; u < P.num_units; u += gridDim.x / P.cl) {
+        WorkIter it;
+        for (it.start(P); it.valid(P); it.next(P)) {
+            const int64_t u = it.u;
             int64_t mb, nb;
             tile_coords(u, P, rank, mb, nb);
             const int64_t row = mb * kBlockM + row_local;
@@ -524,6 +596,92 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 long long ce = P.stats ? clock64() : 0;
                 const bool first = c == 0, last = c == P.k_chunks - 1;
+                if (P.sk && !it.full(P)) {
+                    // ------------- stream-K: this cluster holds k-blocks [kb0, kb1) -------------
+                    // The parts of a unit come from consecutive clusters and are combined as exact
+                    // integers (the same L_g as one CTA over the whole K, so the same C).  A part
+                    // that finds every other part already parked (the usual case: the other
+                    // clusters open their ranges with this unit) is the last: it adds the parked
+                    // int32 partials into its own TMEM accumulators and falls through to the
+                    // normal epilogue.  Otherwise it parks its partial and counts its arrival; the
+                    // last arrival does the same, the others zero and release TMEM.
+                    const int64_t NG = gridDim.x / P.cl, cidx = blockIdx.x / P.cl;
+                    const int64_t nkb = P.num_k_blocks;
+                    const int64_t cf = sk_owner(P, u * nkb, NG), cl_ = sk_owner(P, u * nkb + nkb - 1, NG);
+                    const int np = (int)(cl_ - cf + 1);
+                    const int slot_f = sk_begin(P, cf, NG) == u * nkb ? 0 : 1;
+                    // partial layout [slot][row][used_cols] int32: each thread writes and reads
+                    // its own row with 16-byte accesses
+                    auto part = [&](int64_t cc, int slot) {
+                        return P.sk_part + ((cc * 2 + slot) * P.cl + rank) * (int64_t)P.used_cols *
+                                               kBlockM + (int64_t)row_local * P.used_cols;
+                    };
+                    int *cnt = P.sk_count + u * P.cl + rank;
+                    if (row_local == 0) sk_old = (int)ld_acquire(reinterpret_cast<const unsigned int *>(cnt));
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    bool last_part = sk_old == np - 1;  // every other part is parked
+                    asm volatile("bar.sync 1, 128;" ::: "memory");  // sk_old is reused
+                    if (!last_part) {  // park this part (TMEM untouched until the count is known)
+                        int32_t *mine = part(cidx, it.first ? 0 : 1);
+                        for (uint32_t col = 0; col < P.used_cols; col += 16) {
+                            uint32_t v[16];
+                            __syncwarp();
+                            ptx::tmem_ld_x16(tmem_base + lane_addr + col, v);
+                            ptx::tmem_ld_wait();
+                            int4 *dst = reinterpret_cast<int4 *>(mine + col);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                dst[q] = make_int4((int)v[4 * q], (int)v[4 * q + 1], (int)v[4 * q + 2],
+                                                   (int)v[4 * q + 3]);
+                        }
+                        __threadfence();
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (row_local == 0) sk_old = atomicAdd(cnt, 1);
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        last_part = sk_old == np - 1;
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (!last_part) {  // another part finishes the unit: zero and release TMEM
+                            for (uint32_t col = 0; col < P.used_cols; col += 16)
+                                ptx::tmem_st_zero_x16(tmem_base + lane_addr + col);
+                            ptx::tmem_st_wait();
+                            ptx::tc_fence_before();
+                            ptx::mbar_arrive(tmem_empty);
+                            if (P.stats) st_e += clock64() - ce;
+                            continue;
+                        }
+                    }
+                    // last part: TMEM += every other parked part, column block by column block
+                    // (region totals stay within the INT32 budget of the whole K)
+                    __threadfence();
+                    for (uint32_t col = 0; col < P.used_cols; col += 32) {  // used_cols % 16 == 0
+                        const bool two = col + 16 < P.used_cols;
+                        uint32_t v[32];
+                        __syncwarp();
+                        ptx::tmem_ld_x16(tmem_base + lane_addr + col, v);
+                        if (two) ptx::tmem_ld_x16(tmem_base + lane_addr + col + 16, v + 16);
+                        ptx::tmem_ld_wait();
+                        for (int64_t cc = cf; cc <= cl_; ++cc) {
+                            if (cc == cidx) continue;
+                            const int4 *q0 = reinterpret_cast<const int4 *>(
+                                part(cc, cc == cf ? slot_f : 0) + col);
+                            int4 x[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                x[q] = (q < 4 || two) ? __ldcg(q0 + q) : make_int4(0, 0, 0, 0);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                v[4 * q] += (uint32_t)x[q].x;
+                                v[4 * q + 1] += (uint32_t)x[q].y;
+                                v[4 * q + 2] += (uint32_t)x[q].z;
+                                v[4 * q + 3] += (uint32_t)x[q].w;
+                            }
+                        }
+                        ptx::tmem_st_x16(tmem_base + lane_addr + col, v);
+                        if (two) ptx::tmem_st_x16(tmem_base + lane_addr + col + 16, v + 16);
+                    }
+                    ptx::tmem_st_wait();
+                    // fall through: the unit's complete level sums are in TMEM
+                }
                 if (fp_out && !scr) {
                     // ---------------- fast path: one period, FP64 result ----------------
                     double acc[NC];
@@ -591,6 +749,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                     continue;
                 }
                 // ---------------- general path: K-chunk partials / debug outputs ----------------
+                // K-chunk partial sums live in per-CTA int64 scratch, row-major [row][s N_c], so
+                // each thread moves 16 consecutive values of its row with 16-byte accesses (all
+                // in flight together): a chunk boundary costs a few memory round trips per
+                // level, not one per value.
+                int64_t *scr_row = scr ? scr + (int64_t)row_local * (S * NC) : nullptr;
+                if (scr && !last) {
+                    // drain this K chunk: partial (+)= level sums, TMEM zeroed for the next chunk
+#pragma unroll 1
+                    for (int j = 0; j < S; ++j) {
+                        const bool two = T > 1 && j < S - G;
+#pragma unroll
+                        for (int c0 = 0; c0 < NC; c0 += 16) {
+                            const uint32_t col = (uint32_t)(j * NC + c0);
+                            uint32_t v[16], v2[16];
+                            __syncwarp();
+                            ptx::tmem_ld_x16(tmem_base + lane_addr + col, v);
+                            if (two) ptx::tmem_ld_x16(tmem_base + lane_addr + P.region_col[1] + col, v2);
+                            ptx::tmem_ld_wait();
+                            ptx::tmem_st_zero_x16(tmem_base + lane_addr + col);
+                            if (two) ptx::tmem_st_zero_x16(tmem_base + lane_addr + P.region_col[1] + col);
+                            longlong2 *sp = reinterpret_cast<longlong2 *>(scr_row + col);
+                            longlong2 o[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) o[q] = first ? make_longlong2(0, 0) : sp[q];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                o[q].x += (long long)(int32_t)v[2 * q] + (two ? (int32_t)v2[2 * q] : 0);
+                                o[q].y += (long long)(int32_t)v[2 * q + 1] + (two ? (int32_t)v2[2 * q + 1] : 0);
+                                sp[q] = o[q];
+                            }
+                        }
+                    }
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(tmem_empty);
+                    if (P.stats) st_e += clock64() - ce;
+                    continue;
+                }
                 double acc[NC];
 #pragma unroll
                 for (int i = 0; i < NC; ++i) acc[i] = 0.0;
@@ -599,51 +795,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const bool two = T > 1 && j < S - G;
                     const double sc = pow2(-P.w * (S + 1 - j));
 #pragma unroll
-                    for (int c0 = 0; c0 < NC; c0 += kCH) {
-                        uint32_t v[kCH], v2[kCH];
+                    for (int c0 = 0; c0 < NC; c0 += 16) {
+                        const uint32_t col = (uint32_t)(j * NC + c0);
+                        uint32_t v[16], v2[16];
                         __syncwarp();
-#pragma unroll
-                        for (int c16 = 0; c16 < kCH; c16 += 16) {
-                            if (c0 + c16 >= NC) break;
-                            ptx::tmem_ld_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16),
-                                             &v[c16]);
-                            if (two)
-                                ptx::tmem_ld_x16(tmem_base + lane_addr + P.region_col[1] +
-                                                     (uint32_t)(j * NC + c0 + c16), &v2[c16]);
-                        }
+                        ptx::tmem_ld_x16(tmem_base + lane_addr + col, v);
+                        if (two) ptx::tmem_ld_x16(tmem_base + lane_addr + P.region_col[1] + col, v2);
                         ptx::tmem_ld_wait();
+                        ptx::tmem_st_zero_x16(tmem_base + lane_addr + col);
+                        if (two) ptx::tmem_st_zero_x16(tmem_base + lane_addr + P.region_col[1] + col);
+                        longlong2 o[8];
+                        if (scr && !first) {  // last chunk: the earlier chunks' partials
+                            const longlong2 *sp = reinterpret_cast<const longlong2 *>(scr_row + col);
 #pragma unroll
-                        for (int c16 = 0; c16 < kCH; c16 += 16) {
-                            if (c0 + c16 >= NC) break;
-                            ptx::tmem_st_zero_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c0 + c16));
-                            if (two)
-                                ptx::tmem_st_zero_x16(tmem_base + lane_addr + P.region_col[1] +
-                                                      (uint32_t)(j * NC + c0 + c16));
+                            for (int q = 0; q < 8; ++q) o[q] = sp[q];
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) o[q] = make_longlong2(0, 0);
                         }
 #pragma unroll
-                        for (int ii = 0; ii < kCH; ++ii) {
+                        for (int ii = 0; ii < 16; ++ii) {
                             const int i = c0 + ii;
-                            if (i >= NC) break;
                             int64_t Lg = (int64_t)(int32_t)v[ii];
                             if (two) Lg += (int64_t)(int32_t)v2[ii];
-                            if (scr) {
-                                int64_t *sp = scr + ((int64_t)(j * NC + i) * kBlockM) + row_local;
-                                if (!first) Lg += *sp;
-                                if (!last) {
-                                    *sp = Lg;
-                                    continue;
-                                }
-                            }
+                            Lg += (ii & 1) ? o[ii >> 1].y : o[ii >> 1].x;
                             if (fp_out) {
                                 acc[i] = __fma_rn((double)Lg, sc, acc[i]);
                             } else if (row_ok) {
-                                const int64_t col = nb * NC + i;
-                                if (col < P.n) {
+                                const int64_t colg = nb * NC + i;
+                                if (colg < P.n) {
                                     if (P.mode == EPI_LEVELS_I64)
                                         static_cast<int64_t *>(P.out)[(int64_t)(S - 1 - j) * P.m * P.n +
-                                                                      row + col * P.m] = Lg;
+                                                                      row + colg * P.m] = Lg;
                                     else
-                                        static_cast<int32_t *>(P.out)[row + col * P.m] = (int32_t)Lg;
+                                        static_cast<int32_t *>(P.out)[row + colg * P.m] = (int32_t)Lg;
                                 }
                             }
                         }
@@ -766,7 +951,7 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
             clm = cln = cl = 1;
         } else {
             int64_t c = maxc < p.grid / cl ? maxc : p.grid / cl;
-            c = c < units ? c : units;
+            if (!p.sk) c = c < units ? c : units;  // stream-K: clusters share units' K loops
             grid = (int)(cl * c);
         }
     }
@@ -809,6 +994,11 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.out = a.out;
     P.scratch = p.k_chunks > 1 ? a.chunk_scratch : nullptr;
     P.wave_counter = a.wave_counter;
+    P.sk = (p.sk && p.k_chunks == 1 && a.chunk_scratch) ? 1 : 0;
+    P.sk_total = 0;
+    P.sk_count = nullptr;
+    P.sk_part = nullptr;
+    P.used_cols = (uint32_t)((p.T == 2 ? 2 * S - p.G : S) * NC);
     P.stats = a.stats;
     P.G = p.G;
     P.T = p.T;
@@ -825,6 +1015,16 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.wave_lag = lag_env > 0 ? lag_env : 0;
     static const int ksync_env = getenv("OZIMMU_KSYNC") ? atoi(getenv("OZIMMU_KSYNC")) : 0;
     P.ksync = ksync_env > 0 ? ksync_env : 0;
+    if (P.sk) {
+        // stream-K: no per-wave barrier (no waves); counters zeroed, partials in the scratch
+        P.wave_counter = nullptr;
+        P.sk_total = P.num_units * P.num_k_blocks;
+        P.sk_count = reinterpret_cast<int *>(a.chunk_scratch);
+        const size_t cnt = sk_counters_bytes(P.num_units * cl);
+        P.sk_part = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(a.chunk_scratch) + cnt);
+        e = cudaMemsetAsync(P.sk_count, 0, cnt, st);
+        if (e != cudaSuccess) return e;
+    }
     if (P.wave_counter) {
         e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
         if (e != cudaSuccess) return e;

@@ -104,12 +104,15 @@ struct GemmPlan {
     int grid;
     size_t smem_bytes;
     int tmem_cols;
+    int sk;            // stream-K schedule (small problems; see k_oz_gemm)
+    int64_t tiles;     // stream-K arrival-counter slots (>= units x cluster size)
 };
 
 // Choose tile/pipeline parameters for (s, w, k_pad); returns false if unsupported.
 bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, GemmPlan *p);
 size_t chunk_scratch_bytes(const GemmPlan &p, int s);
 size_t chunk_scratch_bound(const GemmPlan &p, int s, int max_sms);
+size_t sk_counters_bytes(int64_t tiles);
 cudaError_t launch_gemm(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStream_t st,
                         int *launches);
 
