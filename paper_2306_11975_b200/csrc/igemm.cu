@@ -61,6 +61,11 @@ static bool budget_one_chunk(int s, int w, int64_t k_pad, int nc) {
     return G >= 1 && (s + G - 1) / G == 2 && ((int64_t)s + (s - G)) * nc <= 512;
 }
 
+int sk_mode() {
+    static const int m = getenv("OZIMMU_SK") ? atoi(getenv("OZIMMU_SK")) : 0;
+    return m;
+}
+
 bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, GemmPlan *p) {
     if (s < 1 || s > 32 || w < 1) return false;
     int nc = nc_for(s);
@@ -71,7 +76,7 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     // data-parallel schedule at 1024^3-2048^3 (53 -> 90 us and 261 -> 313 us GEMM), the
     // fixup's L2 round trips for a split unit's int32 partials (s N_c values per row) cost
     // more than the partial wave they remove.  Bit-identical either way.
-    static const int sk_env = getenv("OZIMMU_SK") ? atoi(getenv("OZIMMU_SK")) : 0;
+    const int sk_env = sk_mode();
     bool sk = false;
     if (sk_env != 0 && budget_one_chunk(s, w, k_pad, nc)) {
         const int64_t units = ceil_div(m, kBlockM) * ceil_div(ceil_div(n, (int64_t)nc), 2);
@@ -174,9 +179,13 @@ size_t chunk_scratch_bound(const GemmPlan &p, int s, int max_sms) {
     const int g = p.grid > max_sms ? p.grid : max_sms;
     // stream-K may be chosen under any SM cap / for any sub-shape with one pass over K; its
     // counters are bounded by the tiles of the narrowest tile width
-    const size_t skb = sk_scratch(p.tiles * (p.tile_n / 16 > 0 ? p.tile_n / 16 : 1), g);
+    const size_t skb = sk_mode() != 0 ? sk_scratch(p.tiles * (p.tile_n / 16 > 0 ? p.tile_n / 16 : 1), g)
+                                      : 0;
     const int nc = nc_for(s) > p.tile_n ? nc_for(s) : p.tile_n;
-    const size_t kcb = (size_t)g * s * nc * kBlockM * sizeof(int64_t);
+    // K chunks in this plan, or possibly under an SM cap: two INT32 regions that fit TMEM only
+    // thanks to the narrow small-problem tile may not fit with the default width
+    const bool chunks = p.k_chunks > 1 || (p.T == 2 && p.tile_n < nc_for(s));
+    const size_t kcb = chunks ? (size_t)g * s * nc * kBlockM * sizeof(int64_t) : 0;
     return skb > kcb ? skb : kcb;
 }
 
