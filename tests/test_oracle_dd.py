@@ -64,3 +64,41 @@ def test_err_stats_zero_for_exact():
     hi, lo = O.dd_gemm("N", "N", 5, 4, 7, A, 5, B, 7)
     st = O.err_stats(A @ B, hi, lo)
     assert st["max_rel"] == 0.0 and st["mean_rel"] == 0.0
+
+
+def _rn(q):
+    # round-to-nearest-even of an exact rational: Python's Fraction -> float conversion is
+    # correctly rounded (int / int true division), independent of the C code under test
+    return float(q)
+
+
+def test_fp64_gemm_vs_rational_recursive_sum():
+    # fp64_gemm_sub (dd_ref.c) is the CPU "DGEMM" of the accuracy-trend pins; its
+    # definition: acc_0 = 0, acc_l = RN(acc_{l-1} + RN(x_l * y_l)) in ascending l, no FMA.
+    # Checked bit for bit against that recurrence evaluated with exact rationals + one
+    # correctly rounded conversion per operation, for all four transpose combinations and a
+    # row/column subset.
+    m, n, k = 5, 4, 37
+    A = synth.gen_phi(m, k, 2.0, seed=21)
+    B = synth.gen_phi(k, n, 2.0, seed=22)
+    ref = np.zeros((m, n))
+    for i in range(m):
+        for j in range(n):
+            acc = 0.0
+            for l in range(k):
+                acc = _rn(Fraction(acc) + Fraction(_rn(Fraction(float(A[i, l])) *
+                                                        Fraction(float(B[l, j])))))
+            ref[i, j] = acc
+    got = O.fp64_gemm("N", "N", m, n, k, A, m, B, k)
+    assert np.array_equal(got, ref)
+    At = np.asfortranarray(A.T)
+    Bt = np.asfortranarray(B.T)
+    assert np.array_equal(O.fp64_gemm("T", "N", m, n, k, At, k, B, k), ref)
+    assert np.array_equal(O.fp64_gemm("N", "T", m, n, k, A, m, Bt, n), ref)
+    assert np.array_equal(O.fp64_gemm("T", "T", m, n, k, At, k, Bt, n), ref)
+    sub = O.fp64_gemm("N", "N", m, n, k, A, m, B, k, rows=[4, 1], cols=[3, 0, 2])
+    assert np.array_equal(sub, ref[np.ix_([4, 1], [3, 0, 2])])
+    # the order is recursive (not pairwise): a case where the orders differ
+    A1 = np.asfortranarray(np.array([[1.0, 2.0 ** -53, 2.0 ** -53, 2.0 ** -53]]))
+    B1 = np.asfortranarray(np.ones((4, 1)))
+    assert O.fp64_gemm("N", "N", 1, 1, 4, A1, 1, B1, 4)[0, 0] == 1.0  # each tiny add rounds away
