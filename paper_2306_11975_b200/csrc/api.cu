@@ -36,9 +36,9 @@ Layout layout(int64_t m, int64_t n, int64_t k_pad, int s, size_t scratch) {
     L.b_buf = off;
     off += b_buf_bytes(n, k_pad, s);
     L.keys = off;
-    off += align_up(sizeof(int32_t) * (size_t)(m > n ? m : n));
-    L.keys_b = off;  // B's exponent-scan scratch (B is sliced concurrently with A)
-    off += align_up(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    off += align_up(split_scratch_bytes(m > n ? m : n));
+    L.keys_b = off;  // B's slicing scratch (B is sliced concurrently with A)
+    off += align_up(split_scratch_bytes(n));
     L.sync = off;
     off += kAlign;
     L.scratch = off;
@@ -719,7 +719,7 @@ ozimmu_status_t ozimmu_debug_split(ozimmu_handle_t h, ozimmu_op_t op, int is_row
     const int64_t k_pad = round_up(kdim, 16);
     const size_t pbytes = align_up((size_t)num_slices * rows * k_pad);
     void *ws = nullptr;
-    ozimmu_status_t st = get_ws(h, pbytes + align_up(4 * (size_t)rows), &ws);
+    ozimmu_status_t st = get_ws(h, pbytes + align_up(split_scratch_bytes(rows)), &ws);
     if (st) return st;
     int8_t *planes = static_cast<int8_t *>(ws);
     int32_t *keys = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(ws) + pbytes);

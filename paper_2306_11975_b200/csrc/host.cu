@@ -102,7 +102,7 @@ bool host_plan(ozimmu_handle_t h, int64_t m, int64_t n, int64_t k, int s, HostPl
     hp->o_c = off;
     off += align_up((size_t)m * n * sizeof(double));
     hp->o_keys = off;
-    off += align_up(sizeof(int32_t) * (size_t)(mb > nb ? mb : nb));
+    off += align_up(split_scratch_bytes(mb > nb ? mb : nb));
     hp->o_sync = off;
     off += kAlign;
     hp->o_scratch = off;

@@ -92,6 +92,16 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     if (!sk && nc > 32 && s <= 10 &&
         ceil_div(m, kBlockM) * ceil_div(n, (int64_t)nc) <= 5 * (int64_t)num_sms)
         nc = 32;
+    // Short K: a tile's MMAs take only ~num_kb x the epilogue's TMEM drain, which a single
+    // accumulator leaves exposed; two accumulator buffers (2 s N_c <= 512 TMEM columns) let
+    // the next tile's MMAs run during the drain.  For s <= 8 the N_c = 32 instance fits two.
+    const int64_t num_kb0 = ceil_div(k_pad, kKB);
+    static const int acc2_env = getenv("OZIMMU_ACC2") ? atoi(getenv("OZIMMU_ACC2")) : -1;
+    bool acc2 = false;
+    if (!sk && acc2_env != 0) {
+        if (2 * s * nc <= 512) acc2 = true;
+        else if (s <= 8 && (num_kb0 <= 16 || acc2_env == 1)) { nc = 32; acc2 = true; }
+    }
     const size_t smem_budget = 232448 - 3072;  // 227 KB opt-in max minus barriers/align/static
     const size_t b_stage = (size_t)s * nc * kKB;
     const size_t a_stage = (size_t)kBlockM * kKB;
@@ -127,6 +137,8 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
             if (p->chunk_blocks < 1) return false;
         }
     }
+    if (p->T == 2 || p->chunk_blocks < num_kb) acc2 = false;  // one INT32-safe period per tile
+    p->nacc = acc2 ? 2 : 1;
     p->tile_n = nc;
     p->k_block = kKB;
     p->a_stages = a_stages;
@@ -150,10 +162,11 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
         p->grid = (int)(g < num_sms ? g : num_sms);
     }
     p->smem_bytes = 1024 /*align slack*/ + b_stage * b_stages + a_stage * a_stages +
-                    8 * (2 * b_stages + 2 * a_stages + 2) + 16;
+                    8 * (2 * b_stages + 2 * a_stages + 4) + 16;
     int cols = 32;
     const int used = (p->T == 2 ? 2 * s - p->G : s) * nc;
     while (cols < used) cols <<= 1;
+    if (p->nacc == 2) cols *= 2;  // buffer 1 at column cols / 2
     p->tmem_cols = cols;
     return true;
 }

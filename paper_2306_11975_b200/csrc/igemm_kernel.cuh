@@ -57,6 +57,12 @@ struct KParams {
     int *sk_count;               // [num_units][cl] arrivals (zeroed before the launch)
     int32_t *sk_part;            // [G][2 slots][cl][used_cols][128] partial level sums
     uint32_t used_cols;          // TMEM columns holding level sums
+    // accumulator buffers: 2 = the level sums of consecutive tiles alternate between two TMEM
+    // regions acc_stride columns apart, so the MMAs of tile t+1 run while the epilogue drains
+    // tile t (short K: the drain is a large part of a tile); 1 = one region (the epilogue
+    // releases it level by level as soon as every level has been read)
+    int nacc;
+    uint32_t acc_stride;
 };
 
 // ---- work schedule -------------------------------------------------------------------------
@@ -304,9 +310,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *b_empty = b_full + P.b_stages;
     uint64_t *a_full = b_empty + P.b_stages;
     uint64_t *a_empty = a_full + P.a_stages;
-    uint64_t *tmem_full = a_empty + P.a_stages;
-    uint64_t *tmem_empty = tmem_full + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 1);
+    uint64_t *tmem_full = a_empty + P.a_stages;   // [2]: one per accumulator buffer
+    uint64_t *tmem_empty = tmem_full + 2;         // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
     const uint32_t warp = ptx::warp_id();
     const uint32_t lane = ptx::lane_id();
@@ -327,8 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&a_full[i], 1);
             ptx::mbar_init(&a_empty[i], (uint32_t)P.cln);  // the MMAs of each CTA sharing it
         }
-        ptx::mbar_init(tmem_full, 2);  // committed by both MMA issuers
-        ptx::mbar_init(tmem_empty, 4 * 32);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&tmem_full[i], 2);  // committed by both MMA issuers
+            ptx::mbar_init(&tmem_empty[i], 4 * 32);
+        }
         ptx::fence_mbar_init();
         ptx::fence_proxy_async();
     }
@@ -447,9 +455,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kMaxBlk = 256 / NC;  // window blocks per instruction (N <= 256)
         const uint32_t me = warp - 5;
         // TMEM column of A-slice p's window: region t(p) = (p-1)/G (INT32 sub-group)
-        uint32_t pcol[S + 1];
+        uint32_t pcol0[S + 1], pcol[S + 1];
 #pragma unroll
-        for (int p = 1; p <= S; ++p) pcol[p] = tmem_base + P.region_col[(p - 1) / P.G];
+        for (int p = 1; p <= S; ++p) pcol0[p] = tmem_base + P.region_col[(p - 1) / P.G];
         int bs = 0, as = 0;
         uint32_t bph = 0, aph = 0, tpar = 0;
         uint32_t acc_iter = 0;
@@ -484,10 +492,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     kb0 = it.kb0;
                     kb1 = it.kb1;
                 }
-                // the epilogue has read and zeroed the accumulator (phase acc_iter)
+                // the epilogue has read and zeroed accumulator buffer `ab` (its use acc_iter / nacc)
+                const uint32_t ab = P.nacc > 1 ? (acc_iter & 1u) : 0u;
+                const uint32_t acc_ph = P.nacc > 1 ? ((acc_iter >> 1) & 1u) : (acc_iter & 1u);
+#pragma unroll
+                for (int p = 1; p <= S; ++p) pcol[p] = pcol0[p] + ab * P.acc_stride;
                 {
                     long long c0 = P.stats ? clock64() : 0;
-                    ptx::mbar_wait(tmem_empty, acc_iter & 1);
+                    ptx::mbar_wait(&tmem_empty[ab], acc_ph);
                     if (P.stats) st_t += clock64() - c0;
                     ptx::tc_fence_after();
                 }
@@ -537,7 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (++bs == P.b_stages) { bs = 0; bph ^= 1; }
                 }
-                if (ptx::elect_one()) ptx::mma_commit(tmem_full);  // period accumulated
+                if (ptx::elect_one()) ptx::mma_commit(&tmem_full[ab]);  // period accumulated
                 __syncwarp();
             }
         }
@@ -559,6 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // alpha/beta (A8), NaN rows/cols (A9) and the stores of C then overlap those MMAs.
         const uint32_t row_local = warp * 32 + lane;
         const uint32_t lane_addr = (warp * 32) << 16;
+        const uint32_t tmem_base0 = tmem_base;
         int64_t *scr = P.scratch ? P.scratch + (int64_t)blockIdx.x * s * NC * kBlockM : nullptr;
         const int T = P.T;
         const int G = P.G;
@@ -567,10 +580,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // it reads (after reading them) and, once, before the first period.
         {
             const uint32_t used = (uint32_t)(S * NC) + (T > 1 ? (uint32_t)((S - G) * NC) : 0u);
-            for (uint32_t c = 0; c < used; c += 16) ptx::tmem_st_zero_x16(tmem_base + lane_addr + c);
+            for (int b = 0; b < P.nacc; ++b)
+                for (uint32_t c = 0; c < used; c += 16)
+                    ptx::tmem_st_zero_x16(tmem_base + b * P.acc_stride + lane_addr + c);
             ptx::tmem_st_wait();
             ptx::tc_fence_before();
-            ptx::mbar_arrive(tmem_empty);  // phase 0: accumulator zeroed
+            for (int b = 0; b < P.nacc; ++b) ptx::mbar_arrive(&tmem_empty[b]);  // buffers zeroed
         }
         uint32_t acc_iter = 0, tile_iter = 0;
         long long st_e = 0, st_et = 0, st_es = 0;
@@ -592,7 +607,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             asm volatile("bar.sync 1, 128;" ::: "memory");
             ++tile_iter;
             for (int c = 0; c < P.k_chunks; ++c, ++acc_iter) {
-                ptx::mbar_wait(tmem_full, acc_iter & 1);
+                const uint32_t ab = P.nacc > 1 ? (acc_iter & 1u) : 0u;
+                const uint32_t acc_ph = P.nacc > 1 ? ((acc_iter >> 1) & 1u) : (acc_iter & 1u);
+                const uint32_t tmem_base = tmem_base0 + ab * P.acc_stride;  // this period's buffer
+                ptx::mbar_wait(&tmem_full[ab], acc_ph);
                 ptx::tc_fence_after();
                 long long ce = P.stats ? clock64() : 0;
                 const bool first = c == 0, last = c == P.k_chunks - 1;
@@ -645,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ptx::tmem_st_zero_x16(tmem_base + lane_addr + col);
                             ptx::tmem_st_wait();
                             ptx::tc_fence_before();
-                            ptx::mbar_arrive(tmem_empty);
+                            ptx::mbar_arrive(&tmem_empty[ab]);
                             if (P.stats) st_e += clock64() - ce;
                             continue;
                         }
@@ -738,7 +756,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(tmem_empty);  // accumulator read and zeroed: next period may start
+                    ptx::mbar_arrive(&tmem_empty[ab]);  // accumulator read and zeroed: next period may start
                     if (P.stats) st_et += clock64() - ce;
                     long long cs0 = P.stats ? clock64() : 0;
                     if (row_ok) store_row<NC>(P, acc, ebt, ea, row, nb);
@@ -783,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::tmem_st_wait();
                     ptx::tc_fence_before();
-                    ptx::mbar_arrive(tmem_empty);
+                    ptx::mbar_arrive(&tmem_empty[ab]);
                     if (P.stats) st_e += clock64() - ce;
                     continue;
                 }
@@ -836,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(tmem_empty);
+                ptx::mbar_arrive(&tmem_empty[ab]);
                 if (last && fp_out && row_ok) store_row<NC>(P, acc, ebt, ea, row, nb);
                 if (P.stats) st_e += clock64() - ce;
             }
@@ -999,6 +1017,8 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     P.sk_count = nullptr;
     P.sk_part = nullptr;
     P.used_cols = (uint32_t)((p.T == 2 ? 2 * S - p.G : S) * NC);
+    P.nacc = p.nacc;
+    P.acc_stride = (uint32_t)(p.tmem_cols / 2);
     P.stats = a.stats;
     P.G = p.G;
     P.T = p.T;

@@ -12,6 +12,11 @@ constexpr int32_t kKeyEmpty = (int32_t)0x80808080;  // memset(0x80) pattern: "no
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 inline int64_t ceil_div(int64_t x, int64_t a) { return (x + a - 1) / a; }
 
+// launch_split's key_scratch: int32 keys[rows] + per-panel counters (<= rows) + a work counter
+inline size_t split_scratch_bytes(int64_t rows) {
+    return sizeof(int32_t) * (size_t)(2 * (rows > 0 ? rows : 1) + 2);
+}
+
 // A1 (Eq. alpha P:224-227 with l_acc = 31, BPS P:457-460 with l_in = 7):
 // w = min(7, floor((31 - ceil(log2 k)) / 2)) -- the integer form of floor((31 - log2 k)/2).
 inline int slice_width(int64_t k) {
@@ -28,7 +33,9 @@ inline int slice_width(int64_t k) {
 // pidx = reverse ? s - p : p - 1;  elements l in [kdim, k_pad) are written as 0.
 // E[r]: frexp exponent of the vector's max |x| (0 for an all-zero vector,
 // kExpNonFinite if any element is NaN/Inf -- its digits are then all 0).
-// key_scratch: int32[rows] device scratch (strided case only).
+// key_scratch: device scratch of split_scratch_bytes(rows) (exponent keys + the work
+// counters of the one-read fused kernel); may be null only for contiguous vectors with
+// k_pad < 2048 (then the fused kernel is not used).
 // Complex operands (ZGEMM, reading A16): cpx = 1 -> vectors are complex rows of op(A)
 // (kdim / k_pad count doubles: 2 per element, Im negated if conj); cpx = 2 -> vectors are
 // complex columns of op(B), each emitting two plane rows 2r = (Re, -Im, ..) and
@@ -105,6 +112,7 @@ struct GemmPlan {
     size_t smem_bytes;
     int tmem_cols;
     int sk;            // stream-K schedule (small problems; see k_oz_gemm)
+    int nacc;          // accumulator buffers in TMEM (2: short K, see KParams::nacc)
     int64_t tiles;     // stream-K arrival-counter slots (>= units x cluster size)
 };
 

@@ -115,51 +115,112 @@ __device__ __forceinline__ void store_digits(const Digits<W, S> (&dg)[8], int s,
 
 // ---------------------------------------------------------------------------------
 // Fast path for W * S <= 64 (s <= 9 at w = 7): the whole fraction window of an element is
-// one 64-bit word V = floor(|x| 2^(64 - E)) (one variable shift of the significand), digit
-// p is bits [64 - W p, 64 - W (p-1)) of V, and the signs are applied four digits at a time
-// on the packed bytes: for a byte d in [0, 127], -d = (0x80 - d) ^ 0x80 (no borrow leaves
-// the byte), selected by a per-byte mask of the negative elements.
+// one 64-bit word V = floor(|x| 2^(64 - E)), digit p is bits [64 - W p, 64 - W (p-1)) of V.
+// V is formed in floating point: |x| 2^(64-E) is an exact power-of-two scaling (|x| < 2^E,
+// so it is < 2^64; where it would underflow the true value is < 1 and both floors are 0),
+// then one truncating conversion to u64.  The digits of 4 elements are produced 4 at a
+// time: the 4W-bit field of digits 4g+1 .. 4g+4 is spread over 4 bytes with shifts and
+// masks (two levels: 2W-bit halves, then W-bit quarters), and a 4 x 4 byte transpose
+// (8 byte permutes) turns the 4 elements' words into 4 plane words holding one element per
+// byte.  Signs are applied four bytes at a time on the plane words: for a byte d in
+// [0, 127], -d = (0x80 - d) ^ 0x80 (no borrow leaves the byte), selected by a per-byte mask
+// of the negative elements (the sign bits replicated by a byte permute).
 // ---------------------------------------------------------------------------------
+__device__ __forceinline__ double pow2d(int e) {  // 2^e, e in the normal range
+    return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    return __byte_perm(a, b, sel);
+}
+// prmt.b32 with the sign-replicate bit of the selector nibbles honoured (__byte_perm masks
+// the selector to 3 bits per nibble)
+__device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
 template <int W, int S>
 struct Chunk64 {
     static_assert(W * S <= 64, "fraction window must fit 64 bits");
-    uint64_t V[8];
-    uint32_t neg[2];  // 0xFF per byte of a negative element (elements 0-3, 4-7)
+    static constexpr int NG = (S + 3) / 4;  // digit groups of 4
+    uint32_t O[2][S];  // O[h][p-1]: magnitude of digit p of elements 4h .. 4h+3, one per byte
+    uint32_t neg[2];   // 0xFF per byte of a negative element (elements 0-3, 4-7)
 
-    // x[] finite, |x| < 2^E (zeros give V = 0)
+    // bytes q of the result = digit (4g + nd - q), q < nd (nd = digits in group g)
+    template <int Gi>
+    __device__ static __forceinline__ uint32_t spread(uint32_t hi, uint32_t lo) {
+        constexpr int nd = (S - 4 * Gi) < 4 ? (S - 4 * Gi) : 4;
+        constexpr int o = 64 - W * (4 * Gi + nd);  // bit offset of the group's field in V
+        uint32_t y;
+        if constexpr (o >= 32) y = hi >> (o - 32);
+        else if constexpr (o == 0) y = lo;
+        else y = __funnelshift_r(lo, hi, o);
+        constexpr uint32_t m = (1u << W) - 1;
+        if constexpr (nd == 4) {
+            constexpr uint32_t h2 = (1u << (2 * W)) - 1;
+            const uint32_t t = (y & h2) | ((y << (16 - 2 * W)) & (h2 << 16));
+            return (t & (m | (m << 16))) | ((t << (8 - W)) & ((m << 8) | (m << 24)));
+        } else {
+            uint32_t r = y & m;
+            if constexpr (nd > 1) r |= (y << (8 - W)) & (m << 8);
+            if constexpr (nd > 2) r |= (y << (16 - 2 * W)) & (m << 16);
+            return r;
+        }
+    }
+
+    template <int Gi>
+    __device__ __forceinline__ void group(int h, const uint32_t (&hi)[4], const uint32_t (&lo)[4]) {
+        if constexpr (Gi < NG) {
+            constexpr int nd = (S - 4 * Gi) < 4 ? (S - 4 * Gi) : 4;
+            const uint32_t a = spread<Gi>(hi[0], lo[0]), b = spread<Gi>(hi[1], lo[1]);
+            const uint32_t c = spread<Gi>(hi[2], lo[2]), d = spread<Gi>(hi[3], lo[3]);
+            // 4 x 4 byte transpose: o_q = byte q of (a, b, c, d) = digit 4 Gi + nd - q
+            const uint32_t t0 = prmt(a, b, 0x5140), t2 = prmt(c, d, 0x5140);
+            O[h][4 * Gi + nd - 1] = prmt(t0, t2, 0x5410);
+            if constexpr (nd > 1) O[h][4 * Gi + nd - 2] = prmt(t0, t2, 0x7632);
+            if constexpr (nd > 2) {
+                const uint32_t t1 = prmt(a, b, 0x7362), t3 = prmt(c, d, 0x7362);
+                O[h][4 * Gi + nd - 3] = prmt(t1, t3, 0x5410);
+                if constexpr (nd > 3) O[h][4 * Gi] = prmt(t1, t3, 0x7632);
+            }
+            group<Gi + 1>(h, hi, lo);
+        }
+    }
+
+    // x[] finite, |x| < 2^E (zeros give zero digits)
     __device__ __forceinline__ void init(const double (&x)[8], int32_t E) {
-        neg[0] = neg[1] = 0;
+        // 2^(64-E) as one normal double if E >= -958, else as 2^1000 * 2^(64-E-1000)
+        const bool small = E < -958;
+        const double sc1 = small ? 0x1p1000 : pow2d(64 - E);
+        const double sc2 = small ? pow2d(64 - E - 1000) : 1.0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x[i]));
-            const int be = static_cast<int>((u >> 52) & 0x7FF);
-            const uint64_t fr = u & ((1ull << 52) - 1);
-            const uint64_t M = be ? (fr | (1ull << 52)) : fr;  // |x| = M 2^e0
-            const int e0 = be ? be - 1075 : -1074;
-            const int sh = e0 - E + 64;  // V = floor(M 2^sh), sh <= 11 since |x| < 2^E
-            V[i] = sh >= 0 ? (M << sh) : (-sh < 64 ? (M >> -sh) : 0ull);
-            neg[i >> 2] |= (static_cast<uint32_t>(u >> 63) * 0xFFu) << (8 * (i & 3));
+        for (int h = 0; h < 2; ++h) {
+            uint32_t hi[4], lo[4], sg[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const double xe = x[4 * h + e];
+                double y = __dmul_rn(fabs(xe), sc1);
+                if (small) y = __dmul_rn(y, sc2);
+                const unsigned long long V = __double2ull_rz(y);
+                hi[e] = static_cast<uint32_t>(V >> 32);
+                lo[e] = static_cast<uint32_t>(V);
+                sg[e] = static_cast<uint32_t>(__double2hiint(xe));
+            }
+            // sign bit of each element replicated over its byte (prmt sign-extend selectors)
+            neg[h] = prmt(prmt_sx(sg[0], sg[1], 0x00FB), prmt_sx(sg[2], sg[3], 0xFB00), 0x7610);
+            group<0>(h, hi, lo);
         }
     }
     // magnitudes of digit P of elements e0 .. e0+3, one per byte
     template <int P>
     __device__ __forceinline__ uint32_t mags(int e0) const {
-        constexpr int sh = 64 - W * P;
-        uint32_t w = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            w |= (static_cast<uint32_t>(V[e0 + e] >> sh) & ((1u << W) - 1)) << (8 * e);
-        return w;
+        return O[e0 >> 2][P - 1];
     }
-    // swapped pairs (element 2j <-> 2j+1): magnitudes of V[e ^ 1]
+    // swapped pairs (element 2j <-> 2j+1)
     template <int P>
     __device__ __forceinline__ uint32_t mags_swapped(int e0) const {
-        constexpr int sh = 64 - W * P;
-        uint32_t w = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            w |= (static_cast<uint32_t>(V[(e0 + e) ^ 1] >> sh) & ((1u << W) - 1)) << (8 * e);
-        return w;
+        return prmt(O[e0 >> 2][P - 1], 0u, 0x2301);
     }
 };
 
@@ -183,9 +244,11 @@ __device__ __forceinline__ void store_planes64(const Chunk64<W, S> &c, uint32_t 
                 v.x = apply_signs(c.template mags<P>(0), m0);
                 v.y = apply_signs(c.template mags<P>(4), m1);
             }
-            const int pidx = reverse ? (s - P) : (P - 1);
-            *reinterpret_cast<uint2 *>(dst + pidx * plane_stride) = v;
-            store_planes64<W, S, SWAP, P + 1>(c, m0, m1, s, reverse, dst, plane_stride);
+            // dst = plane of slice P; the next slice's plane is plane_stride further (negative
+            // stride for the reversed order, see store64_first)
+            *reinterpret_cast<uint2 *>(dst) = v;
+            store_planes64<W, S, SWAP, P + 1>(c, m0, m1, s, reverse, dst + plane_stride,
+                                              plane_stride);
         }
     }
 }
@@ -196,6 +259,11 @@ __device__ __forceinline__ void emit64(const Chunk64<W, S> &c, int s, int revers
                                        int8_t *planes, int64_t r, int64_t l0, int64_t k_pad,
                                        int64_t plane_stride) {
     constexpr uint32_t kOdd = 0xFF00FF00u, kEven = 0x00FF00FFu;
+    // slice 1's plane, and the signed distance to the next slice's plane
+    if (reverse) {
+        planes += (int64_t)(s - 1) * plane_stride;
+        plane_stride = -plane_stride;
+    }
     if constexpr (CPX == 0) {
         store_planes64<W, S, false>(c, c.neg[0], c.neg[1], s, reverse, planes + r * k_pad + l0,
                                     plane_stride);
@@ -268,6 +336,45 @@ __device__ __forceinline__ void load8(const double *v, int64_t l0, int64_t kdim,
     }
 }
 
+// Exponent key from the running max of the high words |x|_hi (sign cleared): the exponent
+// field of the largest |x| is the largest field, so a normal / non-finite maximum decides E
+// from its field alone; only an all-subnormal (or zero) set needs the exact key of every
+// element (then `exact` is evaluated).
+template <typename F>
+__device__ __forceinline__ int32_t key_from_hi(uint32_t mx, F exact) {
+    if (mx >= 0x7FF00000u) return kExpNonFinite;
+    if (mx >= 0x00100000u) return static_cast<int32_t>(mx >> 20) - 1022;
+    return exact();
+}
+__device__ __forceinline__ uint32_t abs_hi(double x) {
+    return static_cast<uint32_t>(__double2hiint(x)) & 0x7FFFFFFFu;
+}
+
+// Digits of elements l0 .. l0+7 of contiguous vector r (data at v), E = Ev.
+template <int W, int S, int CPX>
+__device__ __forceinline__ void contig_chunk(const double *v, int64_t l0, int64_t kdim, bool al16,
+                                             int32_t Ev, int s, int reverse, int conj,
+                                             int8_t *planes, int64_t r, int64_t k_pad,
+                                             int64_t plane_stride) {
+    const bool bad = Ev == kExpNonFinite;
+    double x[8];
+    if (!bad) load8(v, l0, kdim, al16, x);
+    if constexpr (W * S <= 64) {
+        if (bad) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = 0.0;
+        }
+        Chunk64<W, S> c;
+        c.init(x, bad ? 0 : Ev);
+        emit64<W, S, CPX>(c, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
+    } else {
+        Digits<W, S> dg[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
+        emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // Contiguous vectors (row of op(A) with transA = T, column of op(B) with transB = N):
 // TPR threads per vector, one pass for the exponent (max reduction), one pass for
@@ -297,12 +404,36 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
         // ---- pass 1: E = max exponent key ----
         int32_t key = kKeyEmpty;
         if (active) {
-            for (int64_t c = t; c < nchunk; c += TPR) {
+            // four chunks' loads in flight per thread (memory parallelism with few blocks per
+            // SM, which keeps the vectors in flight -- and so pass 2's re-reads -- in L2); the
+            // max of the high words |x|_hi decides E unless everything is subnormal or zero
+            uint32_t mx = 0;
+            int64_t c = t;
+            for (; c + 3 * TPR < nchunk; c += 4 * TPR) {
+                double x[4][8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) load8(v, (c + u * TPR) * 8, kdim, al16, x[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[u][i]));
+            }
+            for (; c < nchunk; c += TPR) {
                 double x[8];
                 load8(v, c * 8, kdim, al16, x);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
+                for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[i]));
             }
+            key = key_from_hi(mx, [&]() {  // this thread saw only subnormals / zeros: exact
+                int32_t k2 = kKeyEmpty;
+                for (int64_t c2 = t; c2 < nchunk; c2 += TPR) {
+                    double x[8];
+                    load8(v, c2 * 8, kdim, al16, x);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) k2 = max(k2, exp_key(x[i]));
+                }
+                return k2;
+            });
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
@@ -324,28 +455,11 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
                 E[r] = Ev;
             }
         }
-        const bool bad = Ev == kExpNonFinite;
 
         // ---- pass 2: digits ----
-        for (int64_t c = t; c < nchunk; c += TPR) {
-            const int64_t l0 = c * 8;
-            double x[8];
-            if (!bad) load8(v, l0, kdim, al16, x);
-            if constexpr (W * S <= 64) {
-                if (bad) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) x[i] = 0.0;
-                }
-                Chunk64<W, S> c;
-                c.init(x, bad ? 0 : Ev);
-                emit64<W, S, CPX>(c, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
-            } else {
-                Digits<W, S> dg[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-                emit<W, S, CPX>(dg, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
-            }
-        }
+        for (int64_t c = t; c < nchunk; c += TPR)
+            contig_chunk<W, S, CPX>(v, c * 8, kdim, al16, Ev, s, reverse, conj, planes, r, k_pad,
+                                    plane_stride);
     }
 }
 
@@ -404,61 +518,52 @@ __device__ __forceinline__ int tslot(int r, int l) {
     return 2 * (q ^ ((q >> 2) & 7) ^ (r & 7)) + (l & 1);
 }
 
+// One 32-vector x 128-element tile of strided vectors: load (coalesced, transposed through
+// shared memory), then digits of 16 8-element chunks per row.  exps[rr] = E of vector r0+rr
+// (set and published by the caller before the call's first barrier).
 template <int W, int S, int CPX>
-__global__ void __launch_bounds__(256) k_split_strided(const double *__restrict__ M, int64_t ld,
-                                                       int64_t rows, int64_t kdim, int64_t k_pad,
-                                                       int s, int reverse, int conj,
-                                                       const int32_t *__restrict__ keys,
-                                                       int8_t *__restrict__ planes,
-                                                       int64_t plane_stride,
-                                                       int32_t *__restrict__ E,
-                                                       int64_t per_item, int64_t item_stride) {
-    __shared__ __align__(16) double tile[32][128];  // [r][swizzled l]
-    __shared__ int32_t exps[32];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
-    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * 128;
+__device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64_t ld,
+                                             int64_t rows, int64_t kdim, int64_t k_pad, int s,
+                                             int reverse, int conj, int8_t *__restrict__ planes,
+                                             int64_t plane_stride, int64_t per_item,
+                                             int64_t item_stride, int64_t r0, int64_t l0,
+                                             double (*tile)[128], const int32_t *exps) {
     const int tid = threadIdx.x;
-    if (tid < 32) {
-        const int64_t r = r0 + tid;
-        int32_t e = 0;
-        if (r < rows) {
-            e = key_to_exp(keys[r]);
-            if (blockIdx.y == 0) {
-                if (CPX == 2) {
-                    E[2 * r] = e;
-                    E[2 * r + 1] = e;
-                } else {
-                    E[r] = e;
-                }
-            }
-        }
-        exps[tid] = e;
-    }
-    // coalesced load: warp reads 32 consecutive vectors at one l
+    // coalesced load: warp reads 32 consecutive vectors at one l (thread: vector rr,
+    // elements lg + 8 it); interior tiles take the unchecked path
     {
-        const int rr = tid & 31;
+        const int rr = tid & 31, lg = tid >> 5;
         const int64_t r = r0 + rr;
-        const int64_t ro = vec_off(r < rows ? r : 0, 1, per_item, item_stride);
+        const bool rok = r < rows;
+        const int64_t ro = vec_off(rok ? r : 0, 1, per_item, item_stride);
+        double *trow = tile[rr];
         if (CPX) {
             // kdim counts doubles (2 per complex element); complex element (r, lc) is the
             // 16-byte pair at 2 (r + lc ld)
-            const double2 *Mc = reinterpret_cast<const double2 *>(M);
-#pragma unroll 4
+            const double2 *q = reinterpret_cast<const double2 *>(M) + ro + (l0 / 2 + lg) * ld;
+            const int64_t step = 8 * ld;
+            const bool full = rok && l0 + 128 <= kdim;
+#pragma unroll
             for (int it = 0; it < 8; ++it) {
-                const int lc = (tid >> 5) + 8 * it;  // 0..63
-                const int64_t l = l0 + 2 * lc;
+                const int lc = lg + 8 * it;  // 0..63
                 double2 x = make_double2(0.0, 0.0);
-                if (r < rows && l < kdim) x = __ldg(Mc + ro + (l >> 1) * ld);
-                tile[rr][tslot(rr, 2 * lc)] = x.x;
-                tile[rr][tslot(rr, 2 * lc + 1)] = x.y;
+                if (full || (rok && l0 + 2 * lc < kdim)) x = __ldg(q);
+                q += step;
+                trow[tslot(rr, 2 * lc)] = x.x;
+                trow[tslot(rr, 2 * lc + 1)] = x.y;
             }
         } else {
-#pragma unroll 4
+            const double *q = M + ro + (l0 + lg) * ld;
+            const int64_t step = 8 * ld;
+            const bool full = rok && l0 + 128 <= kdim;
+            double x[16];
+#pragma unroll
             for (int it = 0; it < 16; ++it) {
-                const int ll = (tid >> 5) + 8 * it;
-                const int64_t l = l0 + ll;
-                tile[rr][tslot(rr, ll)] = (r < rows && l < kdim) ? __ldg(M + ro + l * ld) : 0.0;
+                x[it] = (full || (rok && l0 + lg + 8 * it < kdim)) ? __ldg(q) : 0.0;
+                q += step;
             }
+#pragma unroll
+            for (int it = 0; it < 16; ++it) trow[tslot(rr, lg + 8 * it)] = x[it];
         }
     }
     __syncthreads();
@@ -495,6 +600,272 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
     }
 }
 
+template <int W, int S, int CPX>
+__global__ void __launch_bounds__(256) k_split_strided(const double *__restrict__ M, int64_t ld,
+                                                       int64_t rows, int64_t kdim, int64_t k_pad,
+                                                       int s, int reverse, int conj,
+                                                       const int32_t *__restrict__ keys,
+                                                       int8_t *__restrict__ planes,
+                                                       int64_t plane_stride,
+                                                       int32_t *__restrict__ E,
+                                                       int64_t per_item, int64_t item_stride) {
+    __shared__ __align__(16) double tile[32][128];  // [r][swizzled l]
+    __shared__ int32_t exps[32];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int64_t l0 = static_cast<int64_t>(blockIdx.y) * 128;
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        const int64_t r = r0 + tid;
+        int32_t e = 0;
+        if (r < rows) {
+            e = key_to_exp(keys[r]);
+            if (blockIdx.y == 0) {
+                if (CPX == 2) {
+                    E[2 * r] = e;
+                    E[2 * r + 1] = e;
+                } else {
+                    E[r] = e;
+                }
+            }
+        }
+        exps[tid] = e;
+    }
+    strided_tile<W, S, CPX>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride,
+                            per_item, item_stride, r0, l0, tile, exps);
+}
+
+// ---------------------------------------------------------------------------------
+// One read of the operand from HBM (large operands): exponent scan and digits in ONE
+// persistent launch.  The vectors are grouped in panels of ~16 MB of input; the work items
+// are, in this order, the scan tiles of panel 0, then for q = 1 .. NP-1 the scan tiles of
+// panel q followed by the slice tiles of panel q-1, then the slice tiles of panel NP-1.
+// A scan tile max-reduces the exponent keys of its elements into keys[r] (atomicMax) and
+// counts itself in done[p]; a slice tile of panel p first waits until done[p] holds all of
+// p's scan tiles.  Between the scan and the slice of an element the GPU reads ~1-2 panels,
+// so the second read of the element hits L2 and HBM sees 8 B read + s B written per
+// element (the two-launch path reads every element twice from HBM at these sizes).
+// Items are claimed in order from an atomic counter, so every claimed item is held by a
+// resident CTA and the scan tiles a slice tile waits for were claimed before it: the waits
+// cannot deadlock whatever else runs on the GPU (e.g. the other operand's slicing on a
+// second stream).  scratch: int32 keys[rows] | done[NP] | claim, all set to 0x80808080
+// by the launcher (= kKeyEmpty for the keys; counters count up from that base).
+// Tiles: strided vectors 32 x 512 (scan) and 32 x 128 (slice, as k_split_strided);
+// contiguous vectors 1 x 4096 for both.
+// ---------------------------------------------------------------------------------
+constexpr uint32_t kCtrBase = 0x80808080u;
+
+struct FusedGeo {
+    int64_t PR;        // vectors per panel (a multiple of 32 for strided vectors)
+    int64_t NP;        // panels
+    int64_t nls, nlb;  // scan / slice l-blocks per vector
+    int64_t TS, TL;    // scan / slice tiles per panel
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t *p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// item -> (slice?, panel, tile)
+__device__ __forceinline__ void fused_item(int64_t i, const FusedGeo &g, bool &slice,
+                                           int64_t &p, int64_t &t) {
+    if (i < g.TS) { slice = false; p = 0; t = i; return; }
+    const int64_t j = i - g.TS, B = g.TS + g.TL;
+    if (j < B * (g.NP - 1)) {
+        const int64_t q = j / B, r = j - q * B;
+        if (r < g.TS) { slice = false; p = q + 1; t = r; }
+        else { slice = true; p = q; t = r - g.TS; }
+        return;
+    }
+    slice = true;
+    p = g.NP - 1;
+    t = j - B * (g.NP - 1);
+}
+
+template <int W, int S, int CPX, bool CONTIG>
+__global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(const double *__restrict__ M, int64_t ld,
+                                                     int64_t rows, int64_t kdim, int64_t k_pad,
+                                                     int s, int reverse, int conj,
+                                                     int8_t *__restrict__ planes,
+                                                     int64_t plane_stride,
+                                                     int32_t *__restrict__ E,
+                                                     int32_t *__restrict__ scratch, FusedGeo g,
+                                                     int64_t per_item, int64_t item_stride) {
+    __shared__ __align__(16) double tile[CONTIG ? 1 : 32][128];
+    __shared__ int32_t red[8][32];
+    __shared__ int32_t exps[32];
+    __shared__ uint32_t next_item[2];
+    int32_t *keys = scratch;
+    uint32_t *done = reinterpret_cast<uint32_t *>(scratch + rows);
+    uint32_t *claim = done + g.NP;
+    const int64_t total = (g.TS + g.TL) * g.NP;
+    const int tid = threadIdx.x;
+    if (tid == 0) next_item[0] = atomicAdd(claim, 1u) - kCtrBase;
+    __syncthreads();
+    int64_t item = next_item[0];
+    for (int iter = 0; item < total; ++iter) {
+        uint32_t nx = 0;
+        if (tid == 0) nx = atomicAdd(claim, 1u);  // next claim in flight while this tile runs
+        bool slice;
+        int64_t p, t;
+        fused_item(item, g, slice, p, t);
+        if (slice) {
+            if (tid == 0) {
+                while (ld_acquire_u32(done + p) - kCtrBase < (uint32_t)g.TS) __nanosleep(64);
+            }
+            __syncthreads();
+        }
+        if constexpr (CONTIG) {
+            // tile: 1 vector x 4096 doubles, chunks c0 = 512 lb + tid and c0 + 256 (8 each)
+            const int64_t vi = t / (slice ? g.nlb : g.nls);
+            const int64_t lb = t - vi * (slice ? g.nlb : g.nls);
+            const int64_t r = p * g.PR + vi;
+            const int64_t c0 = lb * 512 + tid, c1 = c0 + 256;
+            const bool act0 = r < rows && c0 * 8 < k_pad, act1 = r < rows && c1 * 8 < k_pad;
+            const double *v = M + vec_off(r < rows ? r : 0, ld, per_item, item_stride);
+            const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
+            if (!slice) {
+                double x0[8], x1[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x0[i] = x1[i] = 0.0;
+                if (act0) load8(v, c0 * 8, kdim, al16, x0);
+                if (act1) load8(v, c1 * 8, kdim, al16, x1);
+                uint32_t mx = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mx = max(mx, max(abs_hi(x0[i]), abs_hi(x1[i])));
+                int32_t key = key_from_hi(mx, [&]() {
+                    int32_t k2 = kKeyEmpty;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) k2 = max(k2, max(exp_key(x0[i]), exp_key(x1[i])));
+                    return k2;
+                });
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
+                if ((tid & 31) == 0) red[0][tid >> 5] = key;
+                __syncthreads();
+                if (tid == 0) {
+#pragma unroll
+                    for (int i = 1; i < 8; ++i) key = max(key, red[0][i]);
+                    if (r < rows && key != kKeyEmpty) atomicMax(keys + r, key);
+                    red_release_add(done + p, 1u);
+                }
+            } else if (r < rows) {
+                const int32_t Ev = key_to_exp(__ldcg(keys + r));
+                if (tid == 0 && lb == 0) {
+                    if (CPX == 2) {
+                        E[2 * r] = Ev;
+                        E[2 * r + 1] = Ev;
+                    } else {
+                        E[r] = Ev;
+                    }
+                }
+                if (act0)
+                    contig_chunk<W, S, CPX>(v, c0 * 8, kdim, al16, Ev, s, reverse, conj, planes, r,
+                                            k_pad, plane_stride);
+                if (act1)
+                    contig_chunk<W, S, CPX>(v, c1 * 8, kdim, al16, Ev, s, reverse, conj, planes, r,
+                                            k_pad, plane_stride);
+            }
+        } else if (!slice) {
+            // scan tile: 32 vectors x 512 doubles; thread (rr, lane group lg) reads elements
+            // l = l0 + lg + 8 it of vector r0 + rr (a warp reads 32 consecutive vectors)
+            const int64_t rg = t / g.nls;
+            const int64_t r0 = p * g.PR + rg * 32;
+            const int64_t l0 = (t - rg * g.nls) * 512;
+            const int rr = tid & 31, lg = tid >> 5;
+            const int64_t r = r0 + rr;
+            uint32_t mx = 0;
+            int32_t key = kKeyEmpty;
+            if (r < rows) {
+                const int64_t ro = vec_off(r, 1, per_item, item_stride);
+                if (CPX) {  // kdim counts doubles; complex element lc at Mc[ro + lc ld]
+                    const double2 *q = reinterpret_cast<const double2 *>(M) + ro + (l0 / 2 + lg) * ld;
+                    const int64_t kc = kdim / 2 - (l0 / 2 + lg);  // complex elements left
+                    const int64_t step = 8 * ld;
+                    const bool full = kc > 8 * 31;
+#pragma unroll 1
+                    for (int b = 0; b < 4; ++b) {
+                        double2 x[8];
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) {
+                            x[it] = (full || 8 * (8 * b + it) < kc) ? __ldg(q) : make_double2(0.0, 0.0);
+                            q += step;
+                        }
+#pragma unroll
+                        for (int it = 0; it < 8; ++it) mx = max(mx, max(abs_hi(x[it].x), abs_hi(x[it].y)));
+                        if (mx < 0x00100000u) {
+#pragma unroll
+                            for (int it = 0; it < 8; ++it)
+                                key = max(key, max(exp_key(x[it].x), exp_key(x[it].y)));
+                        }
+                    }
+                } else {
+                    const double *q = M + ro + (l0 + lg) * ld;
+                    const int64_t kl = kdim - (l0 + lg);  // elements left from this thread's first
+                    const int64_t step = 8 * ld;
+                    const bool full = kl > 8 * 63;
+#pragma unroll 1
+                    for (int b = 0; b < 4; ++b) {
+                        double x[16];
+#pragma unroll
+                        for (int it = 0; it < 16; ++it) {
+                            x[it] = (full || 8 * (16 * b + it) < kl) ? __ldg(q) : 0.0;
+                            q += step;
+                        }
+#pragma unroll
+                        for (int it = 0; it < 16; ++it) mx = max(mx, abs_hi(x[it]));
+                        if (mx < 0x00100000u) {  // only subnormals / zeros so far: exact keys
+#pragma unroll
+                            for (int it = 0; it < 16; ++it) key = max(key, exp_key(x[it]));
+                        }
+                    }
+                }
+                // a normal / non-finite maximum decides the key; else `key` holds the exact
+                // maximum over the (all subnormal or zero) elements
+                key = key_from_hi(mx, [&]() { return key; });
+            }
+            red[lg][rr] = key;
+            __syncthreads();
+            if (tid < 32) {
+#pragma unroll
+                for (int i = 1; i < 8; ++i) key = max(key, red[i][tid]);
+                if (r < rows && key != kKeyEmpty) atomicMax(keys + r, key);
+            }
+            __syncthreads();
+            if (tid == 0) red_release_add(done + p, 1u);
+        } else {
+            const int64_t rg = t / g.nlb;
+            const int64_t r0 = p * g.PR + rg * 32;
+            const int64_t l0 = (t - rg * g.nlb) * 128;
+            if (tid < 32) {
+                const int64_t r = r0 + tid;
+                int32_t e = 0;
+                if (r < rows) {
+                    e = key_to_exp(__ldcg(keys + r));
+                    if (l0 == 0) {
+                        if (CPX == 2) {
+                            E[2 * r] = e;
+                            E[2 * r + 1] = e;
+                        } else {
+                            E[r] = e;
+                        }
+                    }
+                }
+                exps[tid] = e;
+            }
+            strided_tile<W, S, CPX>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes,
+                                    plane_stride, per_item, item_stride, r0, l0, tile, exps);
+        }
+        if (tid == 0) next_item[(iter + 1) & 1] = nx - kCtrBase;
+        __syncthreads();
+        item = next_item[(iter + 1) & 1];
+    }
+}
+
 }  // namespace
 
 // Exponent keys of strided vectors (element l of vector r at M[r + l ld]; cpx: (re, im)
@@ -507,7 +878,9 @@ cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t ke
     int64_t ysplit = ceil_div(4 * (int64_t)num_sms, rblocks);
     ysplit = ysplit < 1 ? 1 : ysplit;
     int64_t lchunk = round_up(ceil_div(kel, ysplit), 8);
-    if (lchunk < 64) lchunk = 64;
+    // >= 64 elements per thread when that still gives >= 4 blocks per SM (fewer atomics);
+    // small operands take shorter chunks so that every SM has work
+    if (lchunk < 64 && rblocks * ceil_div(kel, 64) >= 4 * (int64_t)num_sms) lchunk = 64;
     ysplit = ceil_div(kel, lchunk);
     if (ysplit < 1) ysplit = 1;
     if (cpx)
@@ -522,12 +895,74 @@ cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t ke
 
 namespace {
 
+template <int W, int S, int CPX, bool CONTIG>
+cudaError_t launch_fused(const double *M, int64_t ld, int64_t rows, int64_t kdim, int64_t k_pad,
+                         int s, bool reverse, int conj, int8_t *planes, int64_t plane_stride,
+                         int32_t *E, int32_t *scratch, int num_sms, cudaStream_t st,
+                         int *launches, BatchMap vm) {
+    // panel size (KB of input), OZIMMU_SPLIT_PANEL_KB (tests use small panels)
+    static const int64_t panel_bytes =
+        (int64_t)(getenv("OZIMMU_SPLIT_PANEL_KB") ? atoi(getenv("OZIMMU_SPLIT_PANEL_KB")) : 16384)
+        << 10;
+    const int64_t vec_bytes = k_pad * 8;
+    int64_t PRt = panel_bytes / vec_bytes;
+    PRt = PRt < 1 ? 1 : PRt;
+    FusedGeo g;
+    if (CONTIG) {
+        g.PR = PRt < rows ? PRt : rows;
+        g.nls = g.nlb = ceil_div(k_pad, 4096);
+        g.NP = ceil_div(rows, g.PR);
+        g.TS = g.TL = g.PR * g.nlb;
+    } else {
+        int64_t PR = PRt / 32 * 32;
+        PR = PR < 32 ? 32 : PR;
+        const int64_t rr = round_up(rows, 32);
+        g.PR = PR < rr ? PR : rr;
+        g.nls = ceil_div(k_pad, 512);
+        g.nlb = ceil_div(k_pad, 128);
+        g.NP = ceil_div(rows, g.PR);
+        g.TS = g.PR / 32 * g.nls;
+        g.TL = g.PR / 32 * g.nlb;
+    }
+    cudaError_t e =
+        cudaMemsetAsync(scratch, 0x80, sizeof(int32_t) * (size_t)(rows + g.NP + 1), st);
+    if (e != cudaSuccess) return e;
+    auto kern = k_split_fused<W, S, CPX, CONTIG>;
+    static int bpsm = 0;  // resident blocks per SM (the grid is persistent)
+    if (bpsm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, kern, 256, 0) != cudaSuccess ||
+            bpsm < 1) {
+            cudaGetLastError();
+            bpsm = 4;
+        }
+    }
+    const int64_t total = (g.TS + g.TL) * g.NP;
+    static const int bps_env =
+        getenv("OZIMMU_SPLIT_FUSED_BPS") ? atoi(getenv("OZIMMU_SPLIT_FUSED_BPS")) : 0;
+    int64_t grid = (int64_t)num_sms * (bps_env > 0 && bps_env < bpsm ? bps_env : bpsm);
+    grid = grid < total ? grid : total;
+    kern<<<(unsigned)grid, 256, 0, st>>>(M, ld, rows, kdim, k_pad, s, reverse ? 1 : 0, conj,
+                                         planes, plane_stride, E, scratch, g, vm.per_item,
+                                         vm.stride);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 template <int W, int S, int CPX>
 cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t rows,
                            int64_t kdim, int64_t k_pad, int s, bool reverse, int conj,
                            int8_t *planes, int64_t plane_stride, int32_t *E, int32_t *key_scratch,
                            int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
     // kdim / k_pad count doubles of the (embedded) vector: 2 per complex element
+    // one-read fused path (k_split_fused) only with OZIMMU_SPLIT_FUSED=1: measured slower than
+    // the two-pass kernels below; it needs contiguous vectors of >= 2048 doubles
+    static const int fused_env =
+        getenv("OZIMMU_SPLIT_FUSED") ? atoi(getenv("OZIMMU_SPLIT_FUSED")) : 0;
+    const bool fused = fused_env && key_scratch && (!contiguous || k_pad >= 2048);
+    if (contiguous && fused)
+        return launch_fused<W, S, CPX, true>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes,
+                                             plane_stride, E, key_scratch, num_sms, st, launches,
+                                             vm);
     if (contiguous) {
         // persistent grid of `bps` blocks per SM (OZIMMU_SPLIT_BPS, default 16 = as many as
         // fit).  Capping the vectors in flight to keep pass 2 in L2 did not pay (16384^2, s = 9:
@@ -551,6 +986,9 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
         return cudaGetLastError();
     }
     // strided: exponent scan then transposing slice
+    if (fused) return launch_fused<W, S, CPX, false>(M, ld, rows, kdim, k_pad, s, reverse, conj,
+                                                      planes, plane_stride, E, key_scratch,
+                                                      num_sms, st, launches, vm);
     cudaError_t e = launch_expscan(M, ld, rows, CPX ? kdim / 2 : kdim, key_scratch, num_sms, st,
                                    launches, CPX ? 1 : 0, vm);
     if (e != cudaSuccess) return e;

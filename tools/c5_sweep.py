@@ -67,10 +67,18 @@ for d in DS:
     for s in SS:
         ms = t_ms(lambda: h.zgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, s), IT)
         rep = h.report()
+        h.timing_enable(2)
+        h.zgemm("N", "N", m, n, k, 1.0, dA, m, dB, k, 0.0, dC, m, s)
+        torch.cuda.synchronize()
+        ph = h.timing_read(2)[-1]
+        h.timing_enable(0)
         print(json.dumps({"d": d, "nq": NQ, "m": m, "n": n, "k": k, "s": s,
                           "ozimmu_tflops": round(fl / ms / 1e9, 2), "ozimmu_ms": round(ms, 3),
                           "cublas_zgemm_tflops": round(fl / cms / 1e9, 2),
                           "cublas_ms": round(cms, 3), "speedup": round(cms / ms, 3),
-                          "tile_n": rep["tile_n"], "auto_picks": picks}), flush=True)
+                          "tile_n": rep["tile_n"], "k_chunks": rep["k_chunks"],
+                          "acc_regions": rep["acc_regions"],
+                          "phases_ms": {kk: round(v, 3) for kk, v in ph.items()},
+                          "auto_picks": picks}), flush=True)
     del psi, U, dA, dB, dC, Am, Bm, Bt
     torch.cuda.empty_cache()
