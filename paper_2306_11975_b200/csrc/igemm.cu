@@ -100,7 +100,9 @@ bool plan_gemm(int s, int w, int64_t m, int64_t n, int64_t k_pad, int num_sms, G
     bool acc2 = false;
     if (!sk && acc2_env != 0) {
         if (2 * s * nc <= 512) acc2 = true;
-        else if (s <= 8 && (num_kb0 <= 16 || acc2_env == 1)) { nc = 32; acc2 = true; }
+        // measured: d = 8 quantum gate (K' = 512, 4 k-blocks) GEMM 13.0 -> 11.7 ms; at 16
+        // k-blocks the narrower tile's MMA mix costs more than the drain (28.6 -> 29.6 ms)
+        else if (s <= 8 && (num_kb0 <= 8 || acc2_env == 1)) { nc = 32; acc2 = true; }
     }
     const size_t smem_budget = 232448 - 3072;  // 227 KB opt-in max minus barriers/align/static
     const size_t b_stage = (size_t)s * nc * kKB;
