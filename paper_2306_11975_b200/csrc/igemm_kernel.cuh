@@ -939,6 +939,13 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
     int clm = 1, cln = 1;
     if (cl_env >= 2 && splits(tiles_n)) cln = 2;
     if (cl_env >= 4 && cln == 2 && splits(tiles_m)) clm = 2;
+    // experiments: OZIMMU_CLUSTER_N / _M set the cluster shape directly (e.g. 4 x 1: A tiles
+    // multicast to four CTAs of a row block)
+    static const int cln_env = getenv("OZIMMU_CLUSTER_N") ? atoi(getenv("OZIMMU_CLUSTER_N")) : 0;
+    static const int clm_env = getenv("OZIMMU_CLUSTER_M") ? atoi(getenv("OZIMMU_CLUSTER_M")) : 0;
+    if (cln_env == 1 || cln_env == 2 || cln_env == 4) cln = cln_env;
+    if (clm_env == 1 || clm_env == 2) clm = clm_env;
+    if (clm * cln > 4) clm = 1;
     int cl = clm * cln;
     if (p.grid < cl) clm = cln = cl = 1;
     int grid = p.grid;

@@ -15,6 +15,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--s", type=int, default=9)
 ap.add_argument("--shapes", default="1024,1536,2048,3072,4096")
+ap.add_argument("--warm-s", type=float, default=0.0,
+                help="seconds of back-to-back calls before timing each shape (clock ramp-up)")
 args = ap.parse_args()
 it = 3 if args.quick else 30
 
@@ -42,6 +44,13 @@ for sz in [int(x) for x in args.shapes.split(",")]:
     for _ in range(3):
         h.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m, args.s)
     torch.cuda.synchronize()
+    if args.warm_s > 0:
+        import time
+        t_end = time.perf_counter() + args.warm_s
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                h.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m, args.s)
+            torch.cuda.synchronize()
     h.timing_enable(it + 1)
     ms = t_ms(lambda: h.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m, args.s), it)
     ph = h.timing_read(it + 1)
