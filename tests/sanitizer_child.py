@@ -1,6 +1,6 @@
 """Child process for tests/test_gpu_sanitizer.py: a few small Ozaki GEMMs through the C ABI
-(ragged tiles, both MMA issuers, CTA pairs, the stream-K fixup and the K-chunked INT32 budget
-path), run under compute-sanitizer.  Prints OK after checking every result against the oracle
+(ragged tiles, both MMA issuers, CTA pairs, the stream-K fixup, the K-chunked INT32 budget
+path and the double-buffered TMEM accumulators), run under compute-sanitizer.  Prints OK after checking every result against the oracle
 (the run also checks that the instrumented kernels still compute the right bits)."""
 import sys
 
@@ -13,7 +13,9 @@ import paper_2306_11975_b200 as oz  # noqa: E402
 import synth  # noqa: E402
 
 CASES = [("N", "N", 256, 192, 512, 9), ("T", "N", 130, 100, 300, 13),
-         ("N", "T", 64, 400, 200, 7), ("N", "N", 40, 24, 140000, 7)]
+         ("N", "T", 64, 400, 200, 7), ("N", "N", 40, 24, 140000, 7),
+         # two TMEM accumulator buffers alternating over several tiles per CTA (short K)
+         ("T", "N", 1500, 640, 256, 4)]
 
 h = oz.Handle(0)
 for i, (ta, tb, m, n, k, s) in enumerate(CASES):
