@@ -39,6 +39,20 @@ __device__ __forceinline__ int32_t exp_key_a(double x) {  // as split.cu's exp_k
     return kKeyEmpty;
 }
 
+// L2 eviction priority of the two passes over a contiguous vector (as split.cu): the exponent
+// pass keeps the vector in L2 for the statistics pass, which reads it for the last time.
+__device__ __forceinline__ uint64_t l2_pol(bool keep) {
+    uint64_t p;
+    if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ldg_pol(const double *q, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(q), "l"(pol));
+    return r;
+}
+
 // (t_last, vlen) of a nonzero finite x relative to the vector exponent E.
 __device__ __forceinline__ void bit_span(double x, int32_t E, int &t_last, int &vlen) {
     const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
@@ -135,6 +149,7 @@ __global__ void __launch_bounds__(256) k_loss_contig(const double *__restrict__ 
                                                      unsigned long long *__restrict__ out) {
     __shared__ int32_t kred[8];
     LossHist H = hist_init(w, s_max);
+    const uint64_t keep = l2_pol(true), strm = l2_pol(false);
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const double *v = M + r * ld;
         int32_t key = kKeyEmpty;
@@ -142,11 +157,11 @@ __global__ void __launch_bounds__(256) k_loss_contig(const double *__restrict__ 
         for (; l + 3 * 256 < kdim; l += 4 * 256) {
             double x[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+            for (int i = 0; i < 4; ++i) x[i] = ldg_pol(v + l + i * 256, keep);
 #pragma unroll
             for (int i = 0; i < 4; ++i) key = max(key, exp_key_a(x[i]));
         }
-        for (; l < kdim; l += 256) key = max(key, exp_key_a(__ldg(v + l)));
+        for (; l < kdim; l += 256) key = max(key, exp_key_a(ldg_pol(v + l, keep)));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
         if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = key;
@@ -160,11 +175,11 @@ __global__ void __launch_bounds__(256) k_loss_contig(const double *__restrict__ 
         for (; l + 3 * 256 < kdim; l += 4 * 256) {
             double x[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+            for (int i = 0; i < 4; ++i) x[i] = ldg_pol(v + l + i * 256, strm);
 #pragma unroll
             for (int i = 0; i < 4; ++i) H.add(x[i], key);
         }
-        for (; l < kdim; l += 256) H.add(__ldg(v + l), key);
+        for (; l < kdim; l += 256) H.add(ldg_pol(v + l, strm), key);
     }
     hist_flush(H, out);
 }
@@ -303,6 +318,7 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
                                                       int32_t *__restrict__ keys_out) {
     __shared__ int32_t kred[8];
     __shared__ unsigned long long red[8][SM + 1];
+    const uint64_t keep = l2_pol(true), strm = l2_pol(false);
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const double *v = M + r * ld;
         int32_t key = kKeyEmpty;
@@ -310,11 +326,11 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
         for (; l + 3 * 256 < kdim; l += 4 * 256) {
             double x[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+            for (int i = 0; i < 4; ++i) x[i] = ldg_pol(v + l + i * 256, keep);
 #pragma unroll
             for (int i = 0; i < 4; ++i) key = max(key, exp_key_a(x[i]));
         }
-        for (; l < kdim; l += 256) key = max(key, exp_key_a(__ldg(v + l)));
+        for (; l < kdim; l += 256) key = max(key, exp_key_a(ldg_pol(v + l, keep)));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
         if ((threadIdx.x & 31) == 0) kred[threadIdx.x >> 5] = key;
@@ -331,11 +347,11 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
         for (; l + 3 * 256 < kdim; l += 4 * 256) {
             double x[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) x[i] = __ldg(v + l + i * 256);
+            for (int i = 0; i < 4; ++i) x[i] = ldg_pol(v + l + i * 256, strm);
 #pragma unroll
             for (int i = 0; i < 4; ++i) acc.add(x[i], key);
         }
-        for (; l < kdim; l += 256) acc.add(__ldg(v + l), key);
+        for (; l < kdim; l += 256) acc.add(ldg_pol(v + l, strm), key);
 #pragma unroll
         for (int t = 0; t <= SM; ++t) {
             unsigned long long x = acc.n[t];

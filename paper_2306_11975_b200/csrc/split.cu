@@ -224,6 +224,15 @@ struct Chunk64 {
     }
 };
 
+__device__ __forceinline__ void st2_hint(int8_t *dst, uint2 v, uint64_t pol, bool use) {
+    if (!use) {
+        *reinterpret_cast<uint2 *>(dst) = v;
+        return;
+    }
+    asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;"
+                 ::"l"(dst), "r"(v.x), "r"(v.y), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ uint32_t apply_signs(uint32_t w, uint32_t m) {
     const uint32_t n = (0x80808080u - w) ^ 0x80808080u;
     return w ^ ((w ^ n) & m);
@@ -233,7 +242,8 @@ __device__ __forceinline__ uint32_t apply_signs(uint32_t w, uint32_t m) {
 template <int W, int S, bool SWAP, int P = 1>
 __device__ __forceinline__ void store_planes64(const Chunk64<W, S> &c, uint32_t m0, uint32_t m1,
                                                int s, int reverse, int8_t *dst,
-                                               int64_t plane_stride) {
+                                               int64_t plane_stride, uint64_t spol = 0,
+                                               bool suse = false) {
     if constexpr (P <= S) {
         if (P <= s) {
             uint2 v;
@@ -246,9 +256,9 @@ __device__ __forceinline__ void store_planes64(const Chunk64<W, S> &c, uint32_t 
             }
             // dst = plane of slice P; the next slice's plane is plane_stride further (negative
             // stride for the reversed order, see store64_first)
-            *reinterpret_cast<uint2 *>(dst) = v;
+            st2_hint(dst, v, spol, suse);
             store_planes64<W, S, SWAP, P + 1>(c, m0, m1, s, reverse, dst + plane_stride,
-                                              plane_stride);
+                                              plane_stride, spol, suse);
         }
     }
 }
@@ -257,7 +267,8 @@ __device__ __forceinline__ void store_planes64(const Chunk64<W, S> &c, uint32_t 
 template <int W, int S, int CPX>
 __device__ __forceinline__ void emit64(const Chunk64<W, S> &c, int s, int reverse, int conj,
                                        int8_t *planes, int64_t r, int64_t l0, int64_t k_pad,
-                                       int64_t plane_stride) {
+                                       int64_t plane_stride, uint64_t spol = 0,
+                                       bool suse = false) {
     constexpr uint32_t kOdd = 0xFF00FF00u, kEven = 0x00FF00FFu;
     // slice 1's plane, and the signed distance to the next slice's plane
     if (reverse) {
@@ -266,21 +277,21 @@ __device__ __forceinline__ void emit64(const Chunk64<W, S> &c, int s, int revers
     }
     if constexpr (CPX == 0) {
         store_planes64<W, S, false>(c, c.neg[0], c.neg[1], s, reverse, planes + r * k_pad + l0,
-                                    plane_stride);
+                                    plane_stride, spol, suse);
     } else if constexpr (CPX == 1) {
         const uint32_t f = conj ? kOdd : 0u;  // conj: Im negated
         store_planes64<W, S, false>(c, c.neg[0] ^ f, c.neg[1] ^ f, s, reverse,
-                                    planes + r * k_pad + l0, plane_stride);
+                                    planes + r * k_pad + l0, plane_stride, spol, suse);
     } else {
         // row 2r = (Re, -Im) (Im := -Im if conj); row 2r+1 = (Im, Re) with the (re, im)
         // swap applied to the masks too
         const uint32_t f0 = conj ? 0u : kOdd;
         store_planes64<W, S, false>(c, c.neg[0] ^ f0, c.neg[1] ^ f0, s, reverse,
-                                    planes + (2 * r) * k_pad + l0, plane_stride);
+                                    planes + (2 * r) * k_pad + l0, plane_stride, spol, suse);
         auto swapb = [](uint32_t m) { return __byte_perm(m, 0, 0x2301); };
         const uint32_t f1 = conj ? kEven : 0u;
         store_planes64<W, S, true>(c, swapb(c.neg[0]) ^ f1, swapb(c.neg[1]) ^ f1, s, reverse,
-                                   planes + (2 * r + 1) * k_pad + l0, plane_stride);
+                                   planes + (2 * r + 1) * k_pad + l0, plane_stride, spol, suse);
     }
 }
 
@@ -320,19 +331,46 @@ __device__ __forceinline__ void emit(Digits<W, S> (&dg)[8], int s, int reverse, 
     }
 }
 
+// L2 eviction priorities (createpolicy + .L2::cache_hint): a first read that will be read again
+// (exponent pass) is kept (evict_last), the second read and the plane stores -- touched once
+// more only by a later kernel -- go first (evict_first), so a vector's second read finds it
+// in L2.  OZIMMU_SPLIT_HINTS=0 turns the hints off (experiments).
+enum : int { HINT_NONE = 0, HINT_KEEP = 1, HINT_STREAM = 2 };
+__device__ __forceinline__ uint64_t l2_policy(int hint) {
+    uint64_t p = 0;
+    if (hint == HINT_KEEP)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else if (hint == HINT_STREAM)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ldg2_hint(const double2 *q, uint64_t pol, bool use) {
+    if (!use) return __ldg(q);
+    double2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(r.x), "=d"(r.y) : "l"(q), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ldg1_hint(const double *q, uint64_t pol, bool use) {
+    if (!use) return __ldg(q);
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(q), "l"(pol));
+    return r;
+}
+
 __device__ __forceinline__ void load8(const double *v, int64_t l0, int64_t kdim, bool al16,
-                                      double (&x)[8]) {
+                                      double (&x)[8], uint64_t pol = 0, bool use = false) {
     if (al16 && l0 + 8 <= kdim) {
         const double2 *q = reinterpret_cast<const double2 *>(v + l0);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            double2 d2 = __ldg(q + i);
+            double2 d2 = ldg2_hint(q + i, pol, use);
             x[2 * i] = d2.x;
             x[2 * i + 1] = d2.y;
         }
     } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = (l0 + i < kdim) ? __ldg(v + l0 + i) : 0.0;
+        for (int i = 0; i < 8; ++i) x[i] = (l0 + i < kdim) ? ldg1_hint(v + l0 + i, pol, use) : 0.0;
     }
 }
 
@@ -355,10 +393,11 @@ template <int W, int S, int CPX>
 __device__ __forceinline__ void contig_chunk(const double *v, int64_t l0, int64_t kdim, bool al16,
                                              int32_t Ev, int s, int reverse, int conj,
                                              int8_t *planes, int64_t r, int64_t k_pad,
-                                             int64_t plane_stride) {
+                                             int64_t plane_stride, uint64_t lpol = 0,
+                                             uint64_t spol = 0, bool use = false) {
     const bool bad = Ev == kExpNonFinite;
     double x[8];
-    if (!bad) load8(v, l0, kdim, al16, x);
+    if (!bad) load8(v, l0, kdim, al16, x, lpol, use);
     if constexpr (W * S <= 64) {
         if (bad) {
 #pragma unroll
@@ -366,7 +405,7 @@ __device__ __forceinline__ void contig_chunk(const double *v, int64_t l0, int64_
         }
         Chunk64<W, S> c;
         c.init(x, bad ? 0 : Ev);
-        emit64<W, S, CPX>(c, s, reverse, conj, planes, r, l0, k_pad, plane_stride);
+        emit64<W, S, CPX>(c, s, reverse, conj, planes, r, l0, k_pad, plane_stride, spol, use);
     } else {
         Digits<W, S> dg[8];
 #pragma unroll
@@ -386,8 +425,13 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
                                                       int s, int reverse, int conj,
                                                       int8_t *__restrict__ planes,
                                                       int64_t plane_stride, int32_t *__restrict__ E,
-                                                      int64_t per_item, int64_t item_stride) {
+                                                      int64_t per_item, int64_t item_stride,
+                                                      int hints) {
     constexpr int VPB = 256 / TPR;  // vectors per block
+    // pass 1 keeps the vector in L2 for pass 2, which reads it for the last time; the planes
+    // are streamed out (see l2_policy)
+    const bool use = hints != 0;
+    const uint64_t keep = use ? l2_policy(HINT_KEEP) : 0, strm = use ? l2_policy(HINT_STREAM) : 0;
     __shared__ int32_t red[256 / 32];
     const int sub = threadIdx.x / TPR;
     const int t = threadIdx.x % TPR;
@@ -412,7 +456,7 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
             for (; c + 3 * TPR < nchunk; c += 4 * TPR) {
                 double x[4][8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) load8(v, (c + u * TPR) * 8, kdim, al16, x[u]);
+                for (int u = 0; u < 4; ++u) load8(v, (c + u * TPR) * 8, kdim, al16, x[u], keep, use);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -420,7 +464,7 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
             }
             for (; c < nchunk; c += TPR) {
                 double x[8];
-                load8(v, c * 8, kdim, al16, x);
+                load8(v, c * 8, kdim, al16, x, keep, use);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[i]));
             }
@@ -459,7 +503,7 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
         // ---- pass 2: digits ----
         for (int64_t c = t; c < nchunk; c += TPR)
             contig_chunk<W, S, CPX>(v, c * 8, kdim, al16, Ev, s, reverse, conj, planes, r, k_pad,
-                                    plane_stride);
+                                    plane_stride, strm, strm, use);
     }
 }
 
@@ -527,7 +571,8 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
                                              int reverse, int conj, int8_t *__restrict__ planes,
                                              int64_t plane_stride, int64_t per_item,
                                              int64_t item_stride, int64_t r0, int64_t l0,
-                                             double (*tile)[128], const int32_t *exps) {
+                                             double (*tile)[128], const int32_t *exps,
+                                             uint64_t pol = 0, bool use = false) {
     const int tid = threadIdx.x;
     // coalesced load: warp reads 32 consecutive vectors at one l (thread: vector rr,
     // elements lg + 8 it); interior tiles take the unchecked path
@@ -547,7 +592,7 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
             for (int it = 0; it < 8; ++it) {
                 const int lc = lg + 8 * it;  // 0..63
                 double2 x = make_double2(0.0, 0.0);
-                if (full || (rok && l0 + 2 * lc < kdim)) x = __ldg(q);
+                if (full || (rok && l0 + 2 * lc < kdim)) x = ldg2_hint(q, pol, use);
                 q += step;
                 trow[tslot(rr, 2 * lc)] = x.x;
                 trow[tslot(rr, 2 * lc + 1)] = x.y;
@@ -559,7 +604,7 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
             double x[16];
 #pragma unroll
             for (int it = 0; it < 16; ++it) {
-                x[it] = (full || (rok && l0 + lg + 8 * it < kdim)) ? __ldg(q) : 0.0;
+                x[it] = (full || (rok && l0 + lg + 8 * it < kdim)) ? ldg1_hint(q, pol, use) : 0.0;
                 q += step;
             }
 #pragma unroll
@@ -590,7 +635,7 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
             }
             Chunk64<W, S> c;
             c.init(x, bad ? 0 : Ev);
-            emit64<W, S, CPX>(c, s, reverse, conj, planes, r, lb, k_pad, plane_stride);
+            emit64<W, S, CPX>(c, s, reverse, conj, planes, r, lb, k_pad, plane_stride, pol, use);
         } else {
             Digits<W, S> dg[8];
 #pragma unroll
@@ -694,7 +739,8 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
                                                      int64_t plane_stride,
                                                      int32_t *__restrict__ E,
                                                      int32_t *__restrict__ scratch, FusedGeo g,
-                                                     int64_t per_item, int64_t item_stride) {
+                                                     int64_t per_item, int64_t item_stride,
+                                                     int hints) {
     __shared__ __align__(16) double tile[CONTIG ? 1 : 32][128];
     __shared__ int32_t red[8][32];
     __shared__ int32_t exps[32];
@@ -704,6 +750,9 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
     uint32_t *claim = done + g.NP;
     const int64_t total = (g.TS + g.TL) * g.NP;
     const int tid = threadIdx.x;
+    // scan reads are kept in L2 for the slice tiles' second (last) read; planes streamed out
+    const bool use = hints != 0;
+    const uint64_t keep = use ? l2_policy(HINT_KEEP) : 0, strm = use ? l2_policy(HINT_STREAM) : 0;
     if (tid == 0) next_item[0] = atomicAdd(claim, 1u) - kCtrBase;
     __syncthreads();
     int64_t item = next_item[0];
@@ -732,8 +781,8 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
                 double x0[8], x1[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) x0[i] = x1[i] = 0.0;
-                if (act0) load8(v, c0 * 8, kdim, al16, x0);
-                if (act1) load8(v, c1 * 8, kdim, al16, x1);
+                if (act0) load8(v, c0 * 8, kdim, al16, x0, keep, use);
+                if (act1) load8(v, c1 * 8, kdim, al16, x1, keep, use);
                 uint32_t mx = 0;
 #pragma unroll
                 for (int i = 0; i < 8; ++i) mx = max(mx, max(abs_hi(x0[i]), abs_hi(x1[i])));
@@ -765,10 +814,10 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
                 }
                 if (act0)
                     contig_chunk<W, S, CPX>(v, c0 * 8, kdim, al16, Ev, s, reverse, conj, planes, r,
-                                            k_pad, plane_stride);
+                                            k_pad, plane_stride, strm, strm, use);
                 if (act1)
                     contig_chunk<W, S, CPX>(v, c1 * 8, kdim, al16, Ev, s, reverse, conj, planes, r,
-                                            k_pad, plane_stride);
+                                            k_pad, plane_stride, strm, strm, use);
             }
         } else if (!slice) {
             // scan tile: 32 vectors x 512 doubles; thread (rr, lane group lg) reads elements
@@ -792,7 +841,8 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
                         double2 x[8];
 #pragma unroll
                         for (int it = 0; it < 8; ++it) {
-                            x[it] = (full || 8 * (8 * b + it) < kc) ? __ldg(q) : make_double2(0.0, 0.0);
+                            x[it] = (full || 8 * (8 * b + it) < kc) ? ldg2_hint(q, keep, use)
+                                                                    : make_double2(0.0, 0.0);
                             q += step;
                         }
 #pragma unroll
@@ -813,7 +863,7 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
                         double x[16];
 #pragma unroll
                         for (int it = 0; it < 16; ++it) {
-                            x[it] = (full || 8 * (16 * b + it) < kl) ? __ldg(q) : 0.0;
+                            x[it] = (full || 8 * (16 * b + it) < kl) ? ldg1_hint(q, keep, use) : 0.0;
                             q += step;
                         }
 #pragma unroll
@@ -858,7 +908,8 @@ __global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(cons
                 exps[tid] = e;
             }
             strided_tile<W, S, CPX>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes,
-                                    plane_stride, per_item, item_stride, r0, l0, tile, exps);
+                                    plane_stride, per_item, item_stride, r0, l0, tile, exps, strm,
+                                    use);
         }
         if (tid == 0) next_item[(iter + 1) & 1] = nx - kCtrBase;
         __syncthreads();
@@ -894,6 +945,11 @@ cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t ke
 }
 
 namespace {
+
+int split_hints() {
+    static const int h = getenv("OZIMMU_SPLIT_HINTS") ? atoi(getenv("OZIMMU_SPLIT_HINTS")) : 1;
+    return h;
+}
 
 template <int W, int S, int CPX, bool CONTIG>
 cudaError_t launch_fused(const double *M, int64_t ld, int64_t rows, int64_t kdim, int64_t k_pad,
@@ -943,7 +999,7 @@ cudaError_t launch_fused(const double *M, int64_t ld, int64_t rows, int64_t kdim
     grid = grid < total ? grid : total;
     kern<<<(unsigned)grid, 256, 0, st>>>(M, ld, rows, kdim, k_pad, s, reverse ? 1 : 0, conj,
                                          planes, plane_stride, E, scratch, g, vm.per_item,
-                                         vm.stride);
+                                         vm.stride, split_hints());
     ++*launches;
     return cudaGetLastError();
 }
@@ -974,13 +1030,13 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
             const int64_t g = rows < cap ? rows : cap;
             k_split_contig<256, W, S, CPX><<<(unsigned)g, 256, 0, st>>>(
                 M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E, vm.per_item,
-                vm.stride);
+                vm.stride, split_hints());
         } else {
             const int64_t nb = ceil_div(rows, 8);
             const int64_t g = nb < 8 * cap ? nb : 8 * cap;
             k_split_contig<32, W, S, CPX><<<(unsigned)g, 256, 0, st>>>(
                 M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride, E, vm.per_item,
-                vm.stride);
+                vm.stride, split_hints());
         }
         ++*launches;
         return cudaGetLastError();

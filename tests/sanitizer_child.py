@@ -1,6 +1,7 @@
 """Child process for tests/test_gpu_sanitizer.py: a few small Ozaki GEMMs through the C ABI
 (ragged tiles, both MMA issuers, CTA pairs, the stream-K fixup, the K-chunked INT32 budget
-path and the double-buffered TMEM accumulators), run under compute-sanitizer.  Prints OK after checking every result against the oracle
+path and the double-buffered TMEM accumulators), run under compute-sanitizer.  Prints OK
+after checking every result against the oracle
 (the run also checks that the instrumented kernels still compute the right bits)."""
 import sys
 
