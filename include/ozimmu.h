@@ -343,6 +343,17 @@ OZIMMU_API ozimmu_status_t ozimmu_debug_level_sums(ozimmu_handle_t h, ozimmu_op_
  * Requires k * max|Ai| * max|Bj| <= 2^31 - 1 (caller's responsibility). */
 OZIMMU_API ozimmu_status_t ozimmu_debug_pair(ozimmu_handle_t h, const int8_t *Ai, const int8_t *Bj,
                                   int64_t m, int64_t n, int64_t k, int32_t *P_out);
+/* Statistics of the accuracy-targeted INT8-AUTO rule (reading A18, Discussion P:713-734) for
+ * the vectors of one operand, as computed on the device before a num_slices = 0 call: rho[t],
+ * t = 0..s_max = max over the vectors (rows of op(M) for is_rows = 1, columns of op(M) for
+ * is_rows = 0; vector layout as ozimmu_debug_split) of the relative l1 truncation residual
+ * after t digits of w bits, ((double)N_t / (double)D) 2^(-wt) from the exact fixed-point sums
+ * N_t = sum ceil(frac(|x| 2^(wt-E)) 2^32), D = sum floor(|x| 2^(32-E)); vectors holding NaN/Inf
+ * or only zeros are skipped (rho = 0 for all t if every vector is).  M: device; rho_out: HOST
+ * double [s_max + 1]; w in [5, 7], s_max in [1, 32].  Synchronises the handle's stream. */
+OZIMMU_API ozimmu_status_t ozimmu_debug_auto_rho(ozimmu_handle_t h, ozimmu_op_t op, int is_rows,
+                                      int64_t rows, int64_t kdim, const double *M, int64_t ld,
+                                      int w, int s_max, double *rho_out);
 
 #ifdef __cplusplus
 }

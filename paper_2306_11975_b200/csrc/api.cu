@@ -700,6 +700,47 @@ ozimmu_status_t ozimmu_dgemm_presliced_b(ozimmu_handle_t h, ozimmu_op_t transA, 
                      OZIMMU_OP_N, nullptr, 0, *beta, C, ldc, num_slices);
 }
 
+ozimmu_status_t ozimmu_debug_auto_rho(ozimmu_handle_t h, ozimmu_op_t op, int is_rows,
+                                      int64_t rows, int64_t kdim, const double *M, int64_t ld,
+                                      int w, int s_max, double *rho_out) {
+    if (!h) return OZIMMU_ERR_NOT_INITIALIZED;
+    if (!valid_op(op) || rows < 0 || kdim < 1 || w < 5 || w > 7 || s_max < 1 ||
+        s_max > kAutoNS - 1 || !rho_out)
+        return OZIMMU_ERR_INVALID_VALUE;
+    if (kdim > OZIMMU_MAX_K) return OZIMMU_ERR_UNSUPPORTED;
+    for (int t = 0; t <= s_max; ++t) rho_out[t] = 0.0;
+    if (rows == 0) return OZIMMU_SUCCESS;
+    if (!M) return OZIMMU_ERR_INVALID_VALUE;
+    const bool contig = is_rows ? (op != OZIMMU_OP_N) : (op == OZIMMU_OP_N);
+    const int64_t min_ld = contig ? kdim : rows;
+    if (ld < (min_ld > 1 ? min_ld : 1)) return OZIMMU_ERR_INVALID_VALUE;
+    if (cudaSetDevice(h->device) != cudaSuccess) return OZIMMU_ERR_CUDA;
+    if (!h->auto_dev &&
+        cudaMalloc(&h->auto_dev, 2 * kAutoNS * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return OZIMMU_ERR_WORKSPACE;
+    }
+    void *ws = nullptr;
+    ozimmu_status_t st = get_ws(h, align_up(trunc_residual_scratch(rows, s_max)), &ws);
+    if (st) return st;
+    int launches = 0;
+    cudaError_t e = cudaMemsetAsync(h->auto_dev, 0, kAutoNS * sizeof(unsigned long long), h->stream);
+    if (e == cudaSuccess)
+        e = launch_trunc_residual(M, ld, contig, rows, kdim, w, s_max, h->auto_dev, ws,
+                                  h->num_sms, h->stream, &launches);
+    unsigned long long bits[kAutoNS];
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(bits, h->auto_dev, sizeof(bits), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) return cuda_status(e);
+    for (int t = 0; t <= s_max; ++t) {
+        double d;
+        memcpy(&d, &bits[t], sizeof(d));
+        rho_out[t] = d;
+    }
+    return OZIMMU_SUCCESS;
+}
+
 ozimmu_status_t ozimmu_debug_split(ozimmu_handle_t h, ozimmu_op_t op, int is_rows, int64_t rows,
                                    int64_t kdim, const double *M, int64_t ld, int num_slices,
                                    int8_t *planes_out, int32_t *exps_out) {

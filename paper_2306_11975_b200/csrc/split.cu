@@ -698,6 +698,9 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
 // contiguous vectors 1 x 4096 for both.
 // ---------------------------------------------------------------------------------
 constexpr uint32_t kCtrBase = 0x80808080u;
+#ifndef OZ_FUSED_MINB
+#define OZ_FUSED_MINB 4  // resident blocks per SM the register allocation targets
+#endif
 
 struct FusedGeo {
     int64_t PR;        // vectors per panel (a multiple of 32 for strided vectors)
@@ -732,7 +735,7 @@ __device__ __forceinline__ void fused_item(int64_t i, const FusedGeo &g, bool &s
 }
 
 template <int W, int S, int CPX, bool CONTIG>
-__global__ void __launch_bounds__(256, (W * S <= 64) ? 4 : 1) k_split_fused(const double *__restrict__ M, int64_t ld,
+__global__ void __launch_bounds__(256, (W * S <= 64) ? OZ_FUSED_MINB : 1) k_split_fused(const double *__restrict__ M, int64_t ld,
                                                      int64_t rows, int64_t kdim, int64_t k_pad,
                                                      int s, int reverse, int conj,
                                                      int8_t *__restrict__ planes,

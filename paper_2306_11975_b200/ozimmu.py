@@ -36,6 +36,7 @@ EXPORTS = [
     "ozimmu_zgemm_strided_batched", "ozimmu_dgemm_host", "ozimmu_set_max_sms",
     "ozimmu_set_auto_accuracy", "ozimmu_nccl_get_unique_id", "ozimmu_nccl_comm_init",
     "ozimmu_nccl_comm_destroy", "ozimmu_set_dist", "ozimmu_dgemm_nccl", "ozimmu_dgemm_bcast",
+    "ozimmu_debug_auto_rho",
 ]
 AUTO_LOSS, AUTO_ACCURACY = 1, 2
 AUTO_SMAX_DEFAULT = 18
@@ -93,6 +94,7 @@ def lib():
         "ozimmu_slice_b": ([H, i32, i64, i64, vp, i64, i32, vp], i32),
         "ozimmu_dgemm_presliced_b": ([H, i32, i64, i64, i64, dp, vp, i64, vp, dp, vp, i64, i32], i32),
         "ozimmu_debug_split": ([H, i32, i32, i64, i64, vp, i64, i32, vp, vp], i32),
+        "ozimmu_debug_auto_rho": ([H, i32, i32, i64, i64, vp, i64, i32, i32, vp], i32),
         "ozimmu_debug_level_sums": ([H, i32, i32, i64, i64, i64, vp, i64, vp, i64, i32, vp], i32),
         "ozimmu_debug_pair": ([H, vp, vp, i64, i64, i64, vp], i32),
         "ozimmu_timing_enable": ([H, i32], i32),
@@ -320,6 +322,14 @@ class Handle:
         _check("ozimmu_debug_split", lib().ozimmu_debug_split(
             self._h, OP[op], int(is_rows), rows, kdim, _ptr(M), ld, int(num_slices),
             _ptr(planes_out), _ptr(exps_out)))
+
+    def debug_auto_rho(self, op, is_rows, rows, kdim, M, ld, w, s_max):
+        """Device statistics of the accuracy AUTO rule for one operand: rho[0..s_max] (numpy)."""
+        out = (ct.c_double * (s_max + 1))()
+        _check("ozimmu_debug_auto_rho", lib().ozimmu_debug_auto_rho(
+            self._h, OP[op], int(is_rows), rows, kdim, _ptr(M), ld, int(w), int(s_max), out))
+        import numpy as _np
+        return _np.array(out[:], dtype=_np.float64)
 
     def debug_level_sums(self, transA, transB, m, n, k, A, lda, B, ldb, num_slices, Lg_out):
         _check("ozimmu_debug_level_sums", lib().ozimmu_debug_level_sums(
