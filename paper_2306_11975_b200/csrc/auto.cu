@@ -241,12 +241,38 @@ __global__ void __launch_bounds__(256) k_loss_strided(const double *__restrict__
 // z = E - e0 - wt fraction bits: the residual after t digits is the low z bits of M.
 template <int W, int SM>  // t = 1..SM (compile time); only t <= s_max are kept
 struct ResidAcc {
-    unsigned long long n[SM + 1];  // [0] = D, [t] = N_t
-    __device__ __forceinline__ void zero() {
+    // Fast path (every element within 43 bits of its vector's maximum, z0 <= 96 below): the
+    // fraction |x| / 2^E is exactly the 96-bit fixed-point V = M 2^(96 - z0) (limbs L0..L2);
+    // digit t leaves the bits below position 96 - wt, the 32 just below the cut are the field
+    // at bit p = 64 - wt, and the rounding-up ("sticky") bit is "V has a set bit below p".
+    // The fields are summed per t in n[t]; the sticky bits are counted once per element in a
+    // per-thread shared-memory histogram over T = the number of cuts above V's lowest set bit
+    // (the element contributes 1 to N_t for t = 1..T), folded into n[] by flush().
+    static constexpr int TMAX = (63 / W) < SM ? (63 / W) : SM;  // cuts with p > 0
+    unsigned long long n[SM + 1];  // [0] = D, [t] = N_t (sticky bits after flush())
+    uint32_t *hist;                // this thread's column: hist[T * 256], T = 1..TMAX
+    double sc;                     // 2^(64 - E): |x| sc is V's top 64 bits plus a fraction
+    bool fp;                       // E >= -958: sc is a normal double, the FP route is exact
+    int32_t E;
+    __device__ __forceinline__ void zero(uint32_t *h, int32_t e) {
 #pragma unroll
         for (int t = 0; t <= SM; ++t) n[t] = 0;
+        hist = h;
+#pragma unroll
+        for (int t = 1; t <= TMAX; ++t) hist[t * 256] = 0;
+        E = e;
+        fp = e >= -958;
+        sc = fp ? __longlong_as_double(static_cast<long long>(1023 + 64 - e) << 52) : 0.0;
     }
-    __device__ __forceinline__ void add(double x, int32_t E) {
+    __device__ __forceinline__ void flush() {
+        uint32_t run = 0;
+#pragma unroll
+        for (int t = TMAX; t >= 1; --t) {
+            run += hist[t * 256];
+            n[t] += run;
+        }
+    }
+    __device__ __forceinline__ void add(double x) {
         const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
         const int be = static_cast<int>((u >> 52) & 0x7FF);
         const uint64_t fr = u & ((1ull << 52) - 1);
@@ -254,21 +280,34 @@ struct ResidAcc {
         if (M == 0) return;
         const int e0 = be ? be - 1075 : -1074;
         const int z0 = E - e0;  // |x| / 2^E = M 2^-z0
-        // floor(M 2^(32 - z0)); for subnormal-only vectors z0 - 32 can be <= 0
-        const int sh = z0 - 32;
-        n[0] += sh <= 0 ? (M << (-sh)) : (sh >= 64 ? 0ull : (M >> sh));
         if (z0 <= 96) {
-            // Fast path (every element within 43 bits of its vector's maximum): the fraction
-            // |x| / 2^E is exactly the 96-bit fixed-point V = M 2^(96 - z0) (limbs L0..L2).
-            // Digit t leaves the bits below position 96 - wt; the 32 just below the cut are
-            // the field at bit p = 64 - wt (one funnel shift, compile-time limbs), and the
-            // rounding-up bit is "V has a set bit below p", i.e. its lowest set bit < p.
-            const int v = 96 - z0;  // 0..95 (M < 2^53 and |x| < 2^E keep V < 2^96)
-            const uint64_t lo = v < 64 ? (M << v) : 0ull;
-            const uint64_t hi = v == 0 ? 0ull : (v < 64 ? (M >> (64 - v)) : (M << (v - 64)));
-            const uint32_t L[3] = {static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32),
-                                   static_cast<uint32_t>(hi)};
-            const int tzpos = __ffsll(static_cast<long long>(M)) - 1 + v;
+            uint32_t L[3];
+            uint64_t V64;
+            if (fp) {
+                // |x| 2^(64-E) < 2^64 exactly (power-of-two scaling); its integer part is V's
+                // top 64 bits and its fraction (exact: <= 53 significant bits) times 2^32 the
+                // low limb, an integer here because no bit of x lies below V's last bit
+                const double y = __dmul_rn(fabs(x), sc);
+                V64 = __double2ull_rz(y);
+                const double r = __dadd_rn(y, -__ull2double_rn(V64));
+                L[0] = __double2uint_rz(__dmul_rn(r, 4294967296.0));
+            } else {
+                const int v = 96 - z0;  // 0..95 (M < 2^53 and |x| < 2^E keep V < 2^96)
+                const uint64_t lo = v < 64 ? (M << v) : 0ull;
+                const uint64_t hi = v == 0 ? 0ull : (v < 64 ? (M >> (64 - v)) : (M << (v - 64)));
+                L[0] = static_cast<uint32_t>(lo);
+                V64 = (lo >> 32) | (hi << 32);
+            }
+            L[1] = static_cast<uint32_t>(V64);
+            L[2] = static_cast<uint32_t>(V64 >> 32);
+            n[0] += L[2];  // floor(|x| 2^(32-E))
+            const int tz = L[0] ? __ffs(static_cast<int>(L[0])) - 1
+                                : 31 + __ffsll(static_cast<long long>(V64));
+            if (tz < 64 - W) {  // at least one cut above the lowest set bit
+                int T = (63 - tz) / W;
+                T = T < TMAX ? T : TMAX;
+                hist[T * 256] += 1u;
+            }
 #pragma unroll
             for (int t = 1; t <= SM; ++t) {
                 const int p = 64 - W * t;
@@ -277,15 +316,16 @@ struct ResidAcc {
                     const int li = p >> 5, bs = p & 31;
                     const uint32_t hiw = li + 1 < 3 ? L[li + 1] : 0u;
                     f = bs ? __funnelshift_r(L[li], hiw, bs) : L[li];
-                    n[t] += static_cast<unsigned long long>(f) + (tzpos < p ? 1ull : 0ull);
                 } else if (p > -32) {
                     f = (L[0] & ((1u << (32 + p)) - 1u)) << (-p);
-                    n[t] += f;
+                } else {
+                    f = 0;
                 }
+                n[t] += f;
             }
             return;
         }
-        // general path: the residual after t digits is the low z bits of M, z = z0 - wt;
+        // general path (floor(|x| 2^(32-E)) = 0 here: z0 > 96): the residual after t digits is the low z bits of M, z = z0 - wt;
         // ceil of its top 32 bits (z > 32: a shift plus a sticky bit)
 #pragma unroll
         for (int t = 1; t <= SM; ++t) {
@@ -316,6 +356,7 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
                                                       int64_t rows, int64_t kdim, int s_max,
                                                       unsigned long long *__restrict__ sums,
                                                       int32_t *__restrict__ keys_out) {
+    __shared__ uint32_t hist_s[(ResidAcc<W, SM>::TMAX + 1) * 256];  // sticky histograms
     __shared__ int32_t kred[8];
     __shared__ unsigned long long red[8][SM + 1];
     const uint64_t keep = l2_pol(true), strm = l2_pol(false);
@@ -342,16 +383,17 @@ __global__ void __launch_bounds__(256) k_resid_contig(const double *__restrict__
         if (threadIdx.x == 0) keys_out[r] = key;
         if (key == kExpNonFinite || key == kKeyEmpty) continue;  // skipped vector
         ResidAcc<W, SM> acc;
-        acc.zero();
+        acc.zero(hist_s + threadIdx.x, key);
         l = threadIdx.x;
         for (; l + 3 * 256 < kdim; l += 4 * 256) {
             double x[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) x[i] = ldg_pol(v + l + i * 256, strm);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc.add(x[i], key);
+            for (int i = 0; i < 4; ++i) acc.add(x[i]);
         }
-        for (; l < kdim; l += 256) acc.add(ldg_pol(v + l, strm), key);
+        for (; l < kdim; l += 256) acc.add(ldg_pol(v + l, strm));
+        acc.flush();
 #pragma unroll
         for (int t = 0; t <= SM; ++t) {
             unsigned long long x = acc.n[t];
@@ -379,19 +421,20 @@ __global__ void __launch_bounds__(256) k_resid_strided(const double *__restrict_
                                                        const int32_t *__restrict__ keys,
                                                        int s_max,
                                                        unsigned long long *__restrict__ sums) {
+    __shared__ uint32_t hist_s[(ResidAcc<W, SM>::TMAX + 1) * 256];  // sticky histograms
     const int64_t r = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
     const int32_t key = r < rows ? keys[r] : kKeyEmpty;
     if (key == kExpNonFinite || key == kKeyEmpty) return;
     ResidAcc<W, SM> acc;
-    acc.zero();
+    acc.zero(hist_s + threadIdx.x, key);
     const int64_t l0 = static_cast<int64_t>(blockIdx.y) * lchunk;
     const int64_t l1 = min(kdim, l0 + lchunk);
     if (CPX) {
         const double2 *Mc = reinterpret_cast<const double2 *>(M);
         for (int64_t l = l0; l < l1; ++l) {
             const double2 z = __ldg(Mc + r + l * ld);
-            acc.add(z.x, key);
-            acc.add(z.y, key);
+            acc.add(z.x);
+            acc.add(z.y);
         }
     } else {
         int64_t l = l0;
@@ -400,10 +443,11 @@ __global__ void __launch_bounds__(256) k_resid_strided(const double *__restrict_
 #pragma unroll
             for (int i = 0; i < 4; ++i) x[i] = __ldg(M + r + (l + i) * ld);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) acc.add(x[i], key);
+            for (int i = 0; i < 4; ++i) acc.add(x[i]);
         }
-        for (; l < l1; ++l) acc.add(__ldg(M + r + l * ld), key);
+        for (; l < l1; ++l) acc.add(__ldg(M + r + l * ld));
     }
+    acc.flush();
 #pragma unroll
     for (int t = 0; t <= SM; ++t) {
         if (t > s_max) break;
