@@ -270,6 +270,35 @@ __device__ __forceinline__ void store_row(const KParams &P, const double (&acc)[
         }
     } else {  // EPI_ZGEMM: columns (2j, 2j+1) = (Re, Im) of complex column j
         const bool beta0 = P.beta == 0.0 && P.beta_im == 0.0;
+        // Fast path (full tiles with normal scales, as for DGEMM): the same operations without
+        // per-element range checks -- X = acc 2^e is one exact multiply -- so the same bits.
+        if ((nb + 1) * NC <= P.n && !P.c_cols.per_item && ea != kExpNonFinite) {
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < NC; ++i) {
+                const long long e = (long long)ea + ebt[i];
+                ok &= ebt[i] != kExpNonFinite && e >= -1022 && e <= 1023;
+            }
+            if (ok) {
+                double2 *cp = reinterpret_cast<double2 *>(P.C) + roff + (nb * NC >> 1) * P.ldc;
+#pragma unroll
+                for (int i = 0; i < NC; i += 2) {
+                    const double xr = __dmul_rn(acc[i], pow2(ea + ebt[i]));
+                    const double xi = __dmul_rn(acc[i + 1], pow2(ea + ebt[i + 1]));
+                    double tr, ti;
+                    cmul(P.alpha, P.alpha_im, xr, xi, tr, ti);
+                    if (!beta0) {
+                        const double2 c = cp[(i >> 1) * P.ldc];
+                        double ur, ui;
+                        cmul(P.beta, P.beta_im, c.x, c.y, ur, ui);
+                        tr = __dadd_rn(tr, ur);
+                        ti = __dadd_rn(ti, ui);
+                    }
+                    cp[(i >> 1) * P.ldc] = make_double2(tr, ti);
+                }
+                return;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < NC; i += 2) {
             const int64_t col = nb * NC + i;

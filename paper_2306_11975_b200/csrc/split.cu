@@ -114,11 +114,12 @@ __device__ __forceinline__ void store_digits(const Digits<W, S> (&dg)[8], int s,
 }
 
 // ---------------------------------------------------------------------------------
-// Fast path for W * S <= 64 (s <= 9 at w = 7): the whole fraction window of an element is
-// one 64-bit word V = floor(|x| 2^(64 - E)), digit p is bits [64 - W p, 64 - W (p-1)) of V.
-// V is formed in floating point: |x| 2^(64-E) is an exact power-of-two scaling (|x| < 2^E,
-// so it is < 2^64; where it would underflow the true value is < 1 and both floors are 0),
-// then one truncating conversion to u64.  The digits of 4 elements are produced 4 at a
+// Fast path for W * S <= 96 (s <= 13 at w = 7): the whole fraction window of an element is
+// one 64-bit word V = floor(|x| 2^(64 - E)) (W S <= 64), or 96 bits (three limbs), and digit
+// p is bits [T - W p, T - W (p-1)) of V (T = 64 or 96).  V is formed in floating point:
+// |x| 2^(64-E) is an exact power-of-two scaling (|x| < 2^E, so it is < 2^64; where it would
+// underflow the true value is < 1 and both floors are 0), then one truncating conversion to
+// u64; the 96-bit window adds the exact fraction times 2^32, truncated, as its low limb.  The digits of 4 elements are produced 4 at a
 // time: the 4W-bit field of digits 4g+1 .. 4g+4 is spread over 4 bytes with shifts and
 // masks (two levels: 2W-bit halves, then W-bit quarters), and a 4 x 4 byte transpose
 // (8 byte permutes) turns the 4 elements' words into 4 plane words holding one element per
@@ -142,20 +143,25 @@ __device__ __forceinline__ uint32_t prmt_sx(uint32_t a, uint32_t b, uint32_t sel
 
 template <int W, int S>
 struct Chunk64 {
-    static_assert(W * S <= 64, "fraction window must fit 64 bits");
+    static_assert(W * S <= 96, "fraction window must fit 96 bits");
+    // limbs of the fraction window: V = floor(|x| 2^(32 NL - E)); W S <= 64 -> 64 bits (the
+    // truncating conversion of |x| 2^(64-E)), else 96 bits (its integer part and the exact
+    // fraction times 2^32, truncated: digits reach at most 91 bits below 2^E)
+    static constexpr int NL = W * S <= 64 ? 2 : 3;
     static constexpr int NG = (S + 3) / 4;  // digit groups of 4
     uint32_t O[2][S];  // O[h][p-1]: magnitude of digit p of elements 4h .. 4h+3, one per byte
     uint32_t neg[2];   // 0xFF per byte of a negative element (elements 0-3, 4-7)
 
     // bytes q of the result = digit (4g + nd - q), q < nd (nd = digits in group g)
     template <int Gi>
-    __device__ static __forceinline__ uint32_t spread(uint32_t hi, uint32_t lo) {
+    __device__ static __forceinline__ uint32_t spread(const uint32_t (&L)[NL]) {
         constexpr int nd = (S - 4 * Gi) < 4 ? (S - 4 * Gi) : 4;
-        constexpr int o = 64 - W * (4 * Gi + nd);  // bit offset of the group's field in V
+        constexpr int o = 32 * NL - W * (4 * Gi + nd);  // bit offset of the group's field in V
+        constexpr int li = o / 32, sh = o % 32;
         uint32_t y;
-        if constexpr (o >= 32) y = hi >> (o - 32);
-        else if constexpr (o == 0) y = lo;
-        else y = __funnelshift_r(lo, hi, o);
+        if constexpr (li + 1 >= NL) y = L[li] >> sh;
+        else if constexpr (sh == 0) y = L[li];
+        else y = __funnelshift_r(L[li], L[li + 1], sh);
         constexpr uint32_t m = (1u << W) - 1;
         if constexpr (nd == 4) {
             constexpr uint32_t h2 = (1u << (2 * W)) - 1;
@@ -170,11 +176,11 @@ struct Chunk64 {
     }
 
     template <int Gi>
-    __device__ __forceinline__ void group(int h, const uint32_t (&hi)[4], const uint32_t (&lo)[4]) {
+    __device__ __forceinline__ void group(int h, const uint32_t (&L)[4][NL]) {
         if constexpr (Gi < NG) {
             constexpr int nd = (S - 4 * Gi) < 4 ? (S - 4 * Gi) : 4;
-            const uint32_t a = spread<Gi>(hi[0], lo[0]), b = spread<Gi>(hi[1], lo[1]);
-            const uint32_t c = spread<Gi>(hi[2], lo[2]), d = spread<Gi>(hi[3], lo[3]);
+            const uint32_t a = spread<Gi>(L[0]), b = spread<Gi>(L[1]);
+            const uint32_t c = spread<Gi>(L[2]), d = spread<Gi>(L[3]);
             // 4 x 4 byte transpose: o_q = byte q of (a, b, c, d) = digit 4 Gi + nd - q
             const uint32_t t0 = prmt(a, b, 0x5140), t2 = prmt(c, d, 0x5140);
             O[h][4 * Gi + nd - 1] = prmt(t0, t2, 0x5410);
@@ -184,7 +190,7 @@ struct Chunk64 {
                 O[h][4 * Gi + nd - 3] = prmt(t1, t3, 0x5410);
                 if constexpr (nd > 3) O[h][4 * Gi] = prmt(t1, t3, 0x7632);
             }
-            group<Gi + 1>(h, hi, lo);
+            group<Gi + 1>(h, L);
         }
     }
 
@@ -196,20 +202,26 @@ struct Chunk64 {
         const double sc2 = small ? pow2d(64 - E - 1000) : 1.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            uint32_t hi[4], lo[4], sg[4];
+            uint32_t L[4][NL], sg[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const double xe = x[4 * h + e];
                 double y = __dmul_rn(fabs(xe), sc1);
                 if (small) y = __dmul_rn(y, sc2);
                 const unsigned long long V = __double2ull_rz(y);
-                hi[e] = static_cast<uint32_t>(V >> 32);
-                lo[e] = static_cast<uint32_t>(V);
+                L[e][NL - 1] = static_cast<uint32_t>(V >> 32);
+                L[e][NL - 2] = static_cast<uint32_t>(V);
+                if constexpr (NL == 3) {
+                    // floor(V 2^32 + frac(y) 2^32): V has <= 53 significant bits (exact as a
+                    // double), so the fraction y - V and its scaling are exact
+                    const double r = __dadd_rn(y, -__ull2double_rn(V));
+                    L[e][0] = __double2uint_rz(__dmul_rn(r, 4294967296.0));
+                }
                 sg[e] = static_cast<uint32_t>(__double2hiint(xe));
             }
             // sign bit of each element replicated over its byte (prmt sign-extend selectors)
             neg[h] = prmt(prmt_sx(sg[0], sg[1], 0x00FB), prmt_sx(sg[2], sg[3], 0xFB00), 0x7610);
-            group<0>(h, hi, lo);
+            group<0>(h, L);
         }
     }
     // magnitudes of digit P of elements e0 .. e0+3, one per byte
@@ -398,7 +410,7 @@ __device__ __forceinline__ void contig_chunk(const double *v, int64_t l0, int64_
     const bool bad = Ev == kExpNonFinite;
     double x[8];
     if (!bad) load8(v, l0, kdim, al16, x, lpol, use);
-    if constexpr (W * S <= 64) {
+    if constexpr (W * S <= 96) {
         if (bad) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) x[i] = 0.0;
@@ -628,7 +640,7 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
             x[2 * h] = d2.x;
             x[2 * h + 1] = d2.y;
         }
-        if constexpr (W * S <= 64) {
+        if constexpr (W * S <= 96) {
             if (bad) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) x[i] = 0.0;
@@ -735,7 +747,7 @@ __device__ __forceinline__ void fused_item(int64_t i, const FusedGeo &g, bool &s
 }
 
 template <int W, int S, int CPX, bool CONTIG>
-__global__ void __launch_bounds__(256, (W * S <= 64) ? OZ_FUSED_MINB : 1) k_split_fused(const double *__restrict__ M, int64_t ld,
+__global__ void __launch_bounds__(256, (W * S <= 96) ? OZ_FUSED_MINB : 1) k_split_fused(const double *__restrict__ M, int64_t ld,
                                                      int64_t rows, int64_t kdim, int64_t k_pad,
                                                      int s, int reverse, int conj,
                                                      int8_t *__restrict__ planes,
@@ -1068,6 +1080,10 @@ cudaError_t launch_split_w(const double *M, int64_t ld, bool contiguous, int64_t
         return launch_split_t<W, 9, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                          planes, plane_stride, E, key_scratch, num_sms, st,
                                          launches, vm);
+    if (s <= 13)  // 96-bit fraction window (W s <= 91): the fast digit path
+        return launch_split_t<W, 13, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
+                                          planes, plane_stride, E, key_scratch, num_sms, st,
+                                          launches, vm);
     if (s <= 16)
         return launch_split_t<W, 16, CPX>(M, ld, contiguous, rows, kdim, k_pad, s, reverse, conj,
                                           planes, plane_stride, E, key_scratch, num_sms, st,
