@@ -338,12 +338,12 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
     // development instrumentation: OZIMMU_STATS=1 -> per-CTA stall counters, dumped below
     static const bool want_stats = getenv("OZIMMU_STATS") != nullptr;
     static long long *stats_buf = nullptr;
-    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 12 * 1024 * sizeof(long long));
+    if (want_stats && !stats_buf) cudaMalloc(&stats_buf, 14 * 1024 * sizeof(long long));
     ga.stats = want_stats ? stats_buf : nullptr;
     cudaError_t e = launch_gemm(ga, gp, EPI_DGEMM, h->stream, launches);
     if (e != cudaSuccess || !ga.stats) return e;
     // development only: synchronous dump of the stall counters
-    constexpr int NS = 12;
+    constexpr int NS = 14;
     static long long host[NS * 1024];
     cudaStreamSynchronize(h->stream);
     cudaMemcpy(host, ga.stats, sizeof(long long) * NS * gp.grid, cudaMemcpyDeviceToHost);
@@ -352,7 +352,7 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
         for (int i = 0; i < NS; ++i) acc[i] += (double)host[c * NS + i];
     const char *names[NS] = {"total", "mma_wait_b", "mma_wait_a", "mma_wait_tmem", "prod_wave",
                              "prod_wait_a", "prod_wait_b", "epi_busy", "epi_tmem", "epi_store",
-                             "mma_wait_a_first_kb", "mma_wait_b_kb0"};
+                             "mma_wait_a_first_kb", "mma_wait_b_kb0", "mma_ns", "unused"};
     fprintf(stderr, "[ozimmu stats] grid=%d avg cycles:", gp.grid);
     for (int i = 0; i < NS; ++i) fprintf(stderr, " %s=%.0f", names[i], acc[i] / gp.grid);
     fprintf(stderr, "\n");

@@ -149,7 +149,7 @@ __host__ __device__ constexpr int slice_p(int S, int i) {
 // stall-counter slots (development instrumentation, OZIMMU_STATS=1)
 enum : int { ST_TOTAL = 0, ST_MMA_WAIT_B, ST_MMA_WAIT_A, ST_MMA_WAIT_TMEM, ST_PROD_WAVE,
              ST_PROD_WAIT_A, ST_PROD_WAIT_B, ST_EPI_BUSY, ST_EPI_TMEM, ST_EPI_STORE,
-             ST_MMA_FIRST_A, ST_MMA_B_TILE0, kStatSlots = 12 };
+             ST_MMA_FIRST_A, ST_MMA_B_TILE0, ST_MMA_NS, ST_KERNEL_NS, kStatSlots = 14 };
 
 // Grouped raster over units (kGroupM row blocks per group); rank = CTA rank in the cluster
 // (rank = rm * cln + rn).  mb / nb may reach tiles_m / tiles_n: a dummy tile (operands
@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t bph = 0, aph = 0, tpar = 0;
         uint32_t acc_iter = 0;
         long long st_b = 0, st_b0 = 0, st_a = 0, st_t = 0, st_af = 0, t_begin = clock64();
+        const uint64_t ns_begin = globaltimer();
         const uint64_t adesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smA));
         const uint64_t bdesc_base = ptx::smem_desc_kmajor<kKB>(ptx::smem_u32(smB));
 
@@ -585,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (P.stats && lane == 0 && me == 0) {
             long long *st = P.stats + (int64_t)blockIdx.x * kStatSlots;
             st[ST_TOTAL] = clock64() - t_begin;
+            st[ST_MMA_NS] = (long long)(globaltimer() - ns_begin);  // with ST_TOTAL: the SM clock
             st[ST_MMA_WAIT_B] = st_b;
             st[ST_MMA_WAIT_A] = st_a;
             st[ST_MMA_WAIT_TMEM] = st_t;
