@@ -573,6 +573,11 @@ def main():
                 "peak_source": f"{peak_src} MEASURED_PEAKS.json; {INT8_PEAK_NOTE}",
                 "gemm_ms": gemm_ms, "slice_ms": slice_ms,
                 "gemm_share_of_step": (gemm_ms / ms) if gemm_ms else None,
+                # the GEMM runs at the board power cap: INT8 work per joule is its real limit
+                "int8_tops_per_watt": (achieved / clk["power_w_median"])
+                if (achieved and clk.get("power_w_median")) else None,
+                "effective_fp64_gflops_per_watt": (value * 1e3 / clk["power_w_median"])
+                if clk.get("power_w_median") else None,
                 "library_context": library_int8_context()}
 
     # ---- cuBLAS DGEMM on the same GPUs (row block, B resident: no communication) -----

@@ -13,7 +13,10 @@ import synth  # noqa: E402
 # debug_split: (op, is_rows, rows, kdim, s); vector r element l = op(M)(r, l) (A) / (l, r) (B)
 SPLITS = [("N", 1, 300, 1000, 9), ("T", 1, 300, 3000, 9), ("N", 0, 77, 2100, 13),
           ("T", 0, 100, 700, 7), ("N", 1, 40, 4097, 17), ("N", 1, 1000, 333, 9),
-          ("T", 1, 33, 20000, 9), ("N", 0, 5, 4096, 20), ("T", 0, 257, 128, 5)]
+          ("T", 1, 33, 20000, 9), ("N", 0, 5, 4096, 20), ("T", 0, 257, 128, 5),
+          # 96-bit fraction window of the fast digit path (10 <= s <= 13 at w = 7)
+          ("N", 1, 70, 700, 10), ("T", 1, 45, 2500, 11), ("N", 0, 90, 3000, 12),
+          ("T", 0, 64, 300, 13)]
 # dgemm: (ta, tb, m, n, k, s)
 DGEMMS = [("N", "N", 300, 200, 5000, 9), ("T", "T", 129, 300, 2500, 13),
           ("N", "T", 64, 70, 20000, 9), ("T", "N", 1, 2049, 2048, 7),
