@@ -1,6 +1,7 @@
 // host.cu -- ozimmu_dgemm_host: the host-buffer entry point (H2D copies, slicing, GEMM and
 // D2H overlapped on three streams; BJ metric "including the matrix splitting" end to end).
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <algorithm>
 #include <vector>
@@ -369,17 +370,20 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     // row blocks already sliced is one GEMM.  The tensor cores start after the first block
     // and chunk, and every C region goes back to the host as soon as its GEMM is done.
     const int64_t P = hp.P, J = hp.J;
-    const int64_t n_ev = 1 + 2 * P + 2 * J + 3 * (P + J);
+    // OZIMMU_HOST_TRACE=1 (development): timing events and a timeline on stderr after the call
+    static const bool trace = getenv("OZIMMU_HOST_TRACE") != nullptr;
+    const int64_t n_ev = 1 + 2 * P + 2 * J + 4 * (P + J);
     cudaEvent_t *ev = static_cast<cudaEvent_t *>(calloc((size_t)n_ev, sizeof(cudaEvent_t)));
     if (!ev) return OZIMMU_ERR_WORKSPACE;
     cudaError_t e = cudaSuccess;
     int64_t made = 0;
     for (; made < n_ev && e == cudaSuccess; ++made)
-        e = cudaEventCreateWithFlags(&ev[made], cudaEventDisableTiming);
+        e = cudaEventCreateWithFlags(&ev[made], trace ? cudaEventDefault : cudaEventDisableTiming);
     cudaEvent_t ev_start = ev[0];
     cudaEvent_t *ev_ain = ev + 1, *ev_afree = ev_ain + P, *ev_bin = ev_afree + P,
                 *ev_bfree = ev_bin + J, *ev_cin = ev_bfree + J, *ev_cdone = ev_cin + (P + J),
-                *ev_cout = ev_cdone + (P + J);
+                *ev_cout = ev_cdone + (P + J), *ev_gstart = ev_cout + (P + J);
+    std::vector<int64_t> reg_shape;  // trace: rows, cols of each region
     int64_t nreg = 0;  // C regions issued
     int launches = 0;
     cudaStream_t cs = h->stream;
@@ -399,6 +403,11 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
             OZ_TRY(copy2d(dCr, m, C + r0 + c0 * ldc, ldc, mr, nc, cudaMemcpyHostToDevice, h->h2d));
             OZ_TRY(cudaEventRecord(ev_cin[q], h->h2d));
             OZ_TRY(cudaStreamWaitEvent(cs, ev_cin[q], 0));
+        }
+        if (trace) {
+            OZ_TRY(cudaEventRecord(ev_gstart[q], cs));
+            reg_shape.push_back(mr);
+            reg_shape.push_back(nc);
         }
         GemmPlan gp;
         if (!plan_gemm(s, w, mr, nc, k_pad, gemm_sms(h), &gp)) {
@@ -452,6 +461,23 @@ extern "C" ozimmu_status_t ozimmu_dgemm_host(ozimmu_handle_t h, ozimmu_op_t tran
     }
     for (int64_t q = 0; q < nreg; ++q) OZ_TRY(cudaStreamWaitEvent(cs, ev_cout[q], 0));
     OZ_TRY(cudaStreamSynchronize(cs));
+    if (trace && e == cudaSuccess) {
+        auto at = [&](cudaEvent_t x) {
+            float ms = -1.f;
+            cudaEventElapsedTime(&ms, ev_start, x);
+            return ms;
+        };
+        for (int64_t i = 0; i < P; ++i)
+            fprintf(stderr, "[host trace] A%lld rows %lld in %.3f\n", (long long)i,
+                    (long long)rows_of(i), at(ev_ain[i]));
+        for (int64_t j = 0; j < J; ++j)
+            fprintf(stderr, "[host trace] B%lld cols %lld in %.3f\n", (long long)j,
+                    (long long)cols_of(j), at(ev_bin[j]));
+        for (int64_t q = 0; q < nreg; ++q)
+            fprintf(stderr, "[host trace] R%lld %lldx%lld gemm %.3f..%.3f out %.3f\n", (long long)q,
+                    (long long)reg_shape[2 * q], (long long)reg_shape[2 * q + 1], at(ev_gstart[q]),
+                    at(ev_cdone[q]), at(ev_cout[q]));
+    }
 #undef OZ_TRY
     if (e != cudaSuccess) {
         cudaStreamSynchronize(h->h2d);
