@@ -561,6 +561,8 @@ def main():
     hw_at_clock = None
     if clk.get("sm_mhz"):
         hw_at_clock = 148 * 8192 * 2 * clk["sm_mhz"] * 1e6 / 1e12  # INT8 MAC/clk/SM x 2 ops
+    s_run = rep.get("num_slices") or s  # the s the library ran (INT8-AUTO: its choice)
+    slice_bytes = (8 + s_run) * (ml * k + k * n) + 4 * (ml + n)
     roofline = {"bound": "tensor", "kernel": "k_oz_gemm (tcgen05.mma.kind::i8 + FP64 epilogue)",
                 "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
                 "frac": (achieved / int8_peak) if achieved else None, "traffic": traffic,
@@ -578,7 +580,17 @@ def main():
                 if (achieved and clk.get("power_w_median")) else None,
                 "effective_fp64_gflops_per_watt": (value * 1e3 / clk["power_w_median"])
                 if clk.get("power_w_median") else None,
-                "library_context": library_int8_context()}
+                "library_context": library_int8_context(),
+                # the slicing phase (A2 + A3): op(A) and op(B) sliced concurrently, HBM-bound;
+                # algorithmic bytes = 8 read + s written per element + 4 per vector, and at N = 1
+                # the strided op(A) of this workload reads A once more for its exponent scan
+                "slicing": ({"bound": "hbm", "ms": slice_ms, "s": s_run,
+                             "algorithmic_bytes": slice_bytes,
+                             "achieved_GBps": slice_bytes / (slice_ms * 1e-3) / 1e9,
+                             "peak_GBps": peaks.get("hbm_gbs"),
+                             "frac": slice_bytes / (slice_ms * 1e-3) / 1e9 / peaks["hbm_gbs"]
+                             if peaks.get("hbm_gbs") else None}
+                            if (slice_ms and world == 1) else None)}
 
     # ---- cuBLAS DGEMM on the same GPUs (row block, B resident: no communication) -----
     cublas = None
