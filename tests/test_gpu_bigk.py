@@ -127,3 +127,27 @@ def test_dgemm_max_k_supported_and_beyond(h):
     with pytest.raises(oz.OzimmuError) as ei:
         h.dgemm("N", "N", m, n, k + 1, 1.0, dA, m, dB, k + 1, 0.0, dC, m, s)
     assert "UNSUPPORTED" in str(ei.value)
+
+
+@pytest.mark.parametrize("k,s", [(70000, 9), (140000, 13)])
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("C", "T")])
+def test_zgemm_bigk_bitexact(h, k, s, ta, tb):
+    """ZGEMM (reading A16: the real embedding has K' = 2k) past 2^17 of K': w = 6 for both
+    sizes, the complex slicing forms at W = 6 (both digit windows: s = 9 -> 64 bits, s = 13 ->
+    96 bits), and the INT32 budget's K chunks; bitwise vs the oracle."""
+    import torch
+    m, n = 24, 10
+    assert O.slice_width(2 * k) == 6
+    A = synth.gen_phi_complex(*_stored(ta, m, k), 0.5, 7101 + k % 31)
+    B = synth.gen_phi_complex(*_stored(tb, k, n), 0.5, 7102 + k % 37)
+    Cin = synth.gen_phi_complex(m, n, 0.5, 7103)
+
+    def z(a):
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, np.complex128).ravel(order="F"))).cuda()
+    dC = z(Cin)
+    h.zgemm(ta, tb, m, n, k, 0.5 - 1.5j, z(A), A.shape[0], z(B), B.shape[0], 0.25j, dC, m, s)
+    torch.cuda.synchronize()
+    assert h.report()["slice_width"] == 6
+    got = dC.cpu().numpy().reshape(n, m).T
+    ref = O.zgemm(ta, tb, m, n, k, 0.5 - 1.5j, A, A.shape[0], B, B.shape[0], 0.25j, Cin, m, s)
+    assert np.array_equal(got, ref)
