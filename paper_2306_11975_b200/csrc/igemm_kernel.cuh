@@ -325,6 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_oz_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const KParams P) {
     constexpr int NC = NCV;  // output columns per tile (nc_for(S), or 32 for small problems)
+#ifndef OZ_PIPE_DRAIN
+#define OZ_PIPE_DRAIN 1
+#endif
+    // epilogue drain with the next level's TMEM loads in flight: N_c = 32 only (measured: 1024^3
+    // GEMM 52.3 -> 51.2 us, 2048^3 257.6 -> 254.7 us; at N_c = 48 the second buffer spills and
+    // 16384^3 loses ~0.5 %)
+    constexpr bool kPipeDrain = OZ_PIPE_DRAIN && NC <= 32;
     __shared__ int32_t eb_s[2][64];  // column exponents of the current tile (double-buffered)
     __shared__ int sk_old;           // stream-K: arrivals before this CTA's part of a unit
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
@@ -736,8 +743,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     double acc[NC];
 #pragma unroll
                     for (int i = 0; i < NC; ++i) acc[i] = 0.0;
+                    // levels held in two INT32 regions first (T = 2: j < S - G), one at a time
+                    const int j_two = T > 1 ? S - G : 0;
 #pragma unroll 1
-                    for (int j = 0; j < S; ++j) {  // level g = s+1-j, descending g
+                    for (int j = 0; j < (kPipeDrain ? j_two : S); ++j) {  // level g = s+1-j
                         const double sc = pow2(-P.w * (S + 1 - j));
                         const bool two = T > 1 && j < S - G;
 #pragma unroll
@@ -783,6 +792,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     if (c0 + ii < NC)
                                         acc[c0 + ii] = __fma_rn((double)(int32_t)v[ii], sc, acc[c0 + ii]);
                             }
+                        }
+                    }
+                    if constexpr (kPipeDrain) {
+                        // the remaining levels (one region each) with the TMEM loads of level j+1
+                        // in flight while level j is zeroed and accumulated (two register
+                        // buffers): the drain is bound by the load latency otherwise, the FP64
+                        // work per level being short (same operations in the same order)
+                        uint32_t va[NC], vb[NC];
+                        auto load_lvl = [&](int j, uint32_t (&v)[NC]) {
+                            __syncwarp();
+#pragma unroll
+                            for (int c16 = 0; c16 < NC; c16 += 16)
+                                ptx::tmem_ld_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c16), &v[c16]);
+                        };
+                        auto use_lvl = [&](int j, const uint32_t (&v)[NC]) {
+#pragma unroll
+                            for (int c16 = 0; c16 < NC; c16 += 16)
+                                ptx::tmem_st_zero_x16(tmem_base + lane_addr + (uint32_t)(j * NC + c16));
+                            const double sc = pow2(-P.w * (S + 1 - j));
+#pragma unroll
+                            for (int ii = 0; ii < NC; ++ii)
+                                acc[ii] = __fma_rn((double)(int32_t)v[ii], sc, acc[ii]);
+                        };
+                        if (j_two < S) load_lvl(j_two, va);
+#pragma unroll 1
+                        for (int j = j_two; j < S; j += 2) {
+                            ptx::tmem_ld_wait();  // level j (va)
+                            if (j + 1 < S) load_lvl(j + 1, vb);
+                            use_lvl(j, va);
+                            if (j + 1 >= S) break;
+                            ptx::tmem_ld_wait();  // level j+1 (vb)
+                            if (j + 2 < S) load_lvl(j + 2, va);
+                            use_lvl(j + 1, vb);
                         }
                     }
                     ptx::tmem_st_wait();
