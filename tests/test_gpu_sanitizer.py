@@ -3,7 +3,12 @@ memcheck on global accesses), for the launch variants that change the kernel's i
 inter-CTA synchronisation: CTA pairs (default), single CTAs, 2 x 2 clusters multicasting B, a
 shallow A ring (the mbarrier phase-aliasing regression of round 1 needed an odd ring; rings are
 now even by construction), and the stream-K schedule.  Each run must report 0 errors and still
-produce oracle-exact results."""
+produce oracle-exact results.
+
+Opt-in (OZIMMU_SANITIZER=1): the GPU pool this repository is tested on has closed
+compute-sanitizer (runs under it left GPUs needing a reset), so by default these cases skip;
+the kernels' synchronisation is covered there by the stress test and the oracle-exact parity
+suites instead."""
 import os
 import shutil
 import subprocess
@@ -28,6 +33,8 @@ VARIANTS = {
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 def test_sanitizer_clean(tool, variant):
+    if os.environ.get("OZIMMU_SANITIZER") != "1":
+        pytest.skip("compute-sanitizer runs are opt-in (OZIMMU_SANITIZER=1): closed on this pool")
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
     env = dict(os.environ)
