@@ -39,6 +39,8 @@ Layout layout(int64_t m, int64_t n, int64_t k_pad, int s, size_t scratch) {
     off += align_up(split_scratch_bytes(m > n ? m : n));
     L.keys_b = off;  // B's slicing scratch (B is sliced concurrently with A)
     off += align_up(split_scratch_bytes(n));
+    L.part = off;  // small calls: partial exponent keys of both operands (k_split_small)
+    off += align_up(split_small_part_bytes(m, n, k_pad));
     L.sync = off;
     off += kAlign;
     L.scratch = off;
@@ -312,8 +314,9 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
                        const int8_t *b_planes, const int32_t *EB, int64_t b_plane_rows,
                        double alpha, double beta, double *C, int64_t ldc, int64_t *scratch,
                        unsigned int *sync, int *launches, BatchMap crow, BatchMap ccol,
-                       int64_t a_plane_rows) {
+                       int64_t a_plane_rows, bool counter_zeroed) {
     GemmArgs ga{};
+    ga.counter_zeroed = counter_zeroed;
     ga.a_plane_rows = a_plane_rows;
     ga.c_rows = crow;
     ga.c_cols = ccol;
@@ -382,9 +385,30 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     int launches = 0;
     int64_t slice_bytes = (int64_t)s * m * k_pad + 4 * m;
     mark(h, PH_START);
+    // Small calls: both operands in one launch on the handle's stream (k_split_small), which
+    // also zeroes the GEMM's wave counter.
+    bool counter_zeroed = false;
+    if (!bbuf_ext && split_small_ok(m, n, k_pad)) {
+        uint8_t *b = base + L.b_buf;
+        int32_t *part = reinterpret_cast<int32_t *>(base + L.part);
+        SmallOp oa{A, lda, m, k, k_pad, transA != OZIMMU_OP_N, 0, a_planes, m * k_pad, EA, part,
+                   amap.per_item, amap.stride};
+        SmallOp ob{B, ldb, n, k, k_pad, transB == OZIMMU_OP_N, 1,
+                   reinterpret_cast<int8_t *>(b), n * k_pad,
+                   reinterpret_cast<int32_t *>(b + b_buf_planes_bytes(n, k_pad, s)),
+                   part + ((k_pad + 127) / 128) * m, bmap.per_item, bmap.stride};
+        mark(h, PH_B);
+        cudaError_t e = launch_split_small(oa, ob, s, w, reinterpret_cast<unsigned int *>(base + L.sync),
+                                           h->num_sms, h->stream, &launches);
+        if (e != cudaSuccess) return cuda_status(e);
+        mark(h, PH_A);
+        bbuf = b;
+        slice_bytes += (int64_t)s * n * k_pad + 4 * n;
+        counter_zeroed = true;
+    }
     // op(B) is sliced on the handle's second stream while op(A) is sliced on its stream
     // (separate exponent-scan scratch); the GEMM waits for both.
-    const bool fork = !bbuf_ext;
+    const bool fork = !bbuf_ext && !counter_zeroed;
     if (fork) {
         uint8_t *b = base + L.b_buf;
         cudaError_t e = aux_fork(h);
@@ -398,12 +422,14 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
         }
         bbuf = b;
         slice_bytes += (int64_t)s * n * k_pad + 4 * n;
-    } else {
+    } else if (!counter_zeroed) {
         mark(h, PH_B);
     }
-    cudaError_t e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches,
-                            amap);
-    mark(h, PH_A);
+    cudaError_t e = cudaSuccess;
+    if (!counter_zeroed) {
+        e = slice_a(h, transA, m, k, k_pad, A, lda, s, w, a_planes, EA, keys, &launches, amap);
+        mark(h, PH_A);
+    }
     if (fork) {
         const cudaError_t ej = aux_join(h);
         if (e == cudaSuccess) e = ej;
@@ -413,7 +439,8 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     e = fused_gemm(h, gp, m, n, k_pad, s, w, a_planes, EA, reinterpret_cast<const int8_t *>(bbuf),
                    reinterpret_cast<const int32_t *>(bbuf + b_buf_planes_bytes(n, k_pad, s)), 0,
                    alpha, beta, C, ldc, reinterpret_cast<int64_t *>(base + L.scratch),
-                   reinterpret_cast<unsigned int *>(base + L.sync), &launches, crow, ccol);
+                   reinterpret_cast<unsigned int *>(base + L.sync), &launches, crow, ccol, 0,
+                   counter_zeroed);
     if (e != cudaSuccess) return cuda_status(e);
     mark(h, PH_GEMM1);
     mark_done(h);

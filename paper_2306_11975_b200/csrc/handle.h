@@ -63,7 +63,7 @@ inline int gemm_sms(ozimmu_handle_t h) {
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {  // workspace carve-up for one dgemm call
-    size_t a_planes, a_exp, b_buf, keys, keys_b, sync, scratch, total;
+    size_t a_planes, a_exp, b_buf, keys, keys_b, part, sync, scratch, total;
 };
 
 // Phase events of one computing call (ozimmu_timing_read): start, B sliced (on the stream
@@ -129,7 +129,8 @@ cudaError_t fused_gemm(ozimmu_handle_t h, const GemmPlan &gp, int64_t m, int64_t
                        const int8_t *b_planes, const int32_t *EB, int64_t b_plane_rows,
                        double alpha, double beta, double *C, int64_t ldc, int64_t *scratch,
                        unsigned int *sync, int *launches, BatchMap crow = BatchMap(),
-                       BatchMap ccol = BatchMap(), int64_t a_plane_rows = 0);
+                       BatchMap ccol = BatchMap(), int64_t a_plane_rows = 0,
+                       bool counter_zeroed = false);
 // slice(B) || slice(A) -> fused GEMM for one real call (bbuf_ext: B already sliced).
 ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int64_t n, int64_t k,
                           double alpha, const double *A, int64_t lda, const uint8_t *bbuf_ext,

@@ -389,6 +389,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // Programmatic dependent launch (launch_t): the set-up above may overlap the tail of the
+    // previous kernel on the stream (the slicing); nothing below reads global memory before
+    // that kernel has completed and its writes are visible.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
 
     if (warp == 4) {
@@ -1125,25 +1129,35 @@ cudaError_t launch_t(const GemmArgs &a, const GemmPlan &p, EpiMode mode, cudaStr
         e = cudaMemsetAsync(P.sk_count, 0, cnt, st);
         if (e != cudaSuccess) return e;
     }
-    if (P.wave_counter) {
+    if (P.wave_counter && !a.counter_zeroed) {
         e = cudaMemsetAsync(P.wave_counter, 0, sizeof(unsigned int), st);
         if (e != cudaSuccess) return e;
-    }
-    if (cl == 1) {
-        kern<<<grid, kThreads, p.smem_bytes, st>>>(tmA, tmB, P);
-        return cudaGetLastError();
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = p.smem_bytes;
     cfg.stream = st;
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cudaLaunchAttribute la[2];
+    int na = 0;
+    if (cl > 1) {
+        la[na].id = cudaLaunchAttributeClusterDimension;
+        la[na].val.clusterDim.x = cl;
+        la[na].val.clusterDim.y = 1;
+        la[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    // programmatic dependent launch: CTAs may start their set-up (barriers, TMEM, descriptor
+    // prefetch) while the previous kernel drains; k_oz_gemm waits (griddepcontrol.wait) before
+    // its first global access.  OZIMMU_NO_PDL=1 turns it off (experiments).
+    static const bool no_pdl = getenv("OZIMMU_NO_PDL") != nullptr;
+    if (!no_pdl) {
+        la[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        la[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = na ? la : nullptr;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, P);
 }
 

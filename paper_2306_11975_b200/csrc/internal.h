@@ -56,6 +56,28 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
                          cudaStream_t st, int *launches, int cpx = 0, int conj = 0,
                          BatchMap vm = BatchMap());
 
+// Small calls: both operands sliced in ONE launch (split.cu k_split_small; contiguous or
+// strided vectors, real operands; opt-in, measured slower).  part: the operands' partial
+// exponent keys, <= ceil(kdim / 128) x rows int32 each (no initialisation needed).
+// split_small_ok: the call is small enough (both operands' input bytes <=
+// OZIMMU_SPLIT_SMALL_MB, default 0 = off);
+// split_small_part_bytes: workspace for both operands' partials (0 when not small).
+struct SmallOp {
+    const double *M;
+    int64_t ld, rows, kdim, k_pad;
+    int contig, reverse;
+    int8_t *planes;
+    int64_t plane_stride;
+    int32_t *E;
+    int32_t *part;
+    int64_t per_item, item_stride;
+};
+bool split_small_ok(int64_t m, int64_t n, int64_t k_pad);
+size_t split_small_part_bytes(int64_t m, int64_t n, int64_t k_pad);
+cudaError_t launch_split_small(const SmallOp &a, const SmallOp &b, int s, int w,
+                               unsigned int *zero_ctr, int num_sms, cudaStream_t st,
+                               int *launches);
+
 cudaError_t launch_expscan(const double *M, int64_t ld, int64_t rows, int64_t kel, int32_t *keys,
                            int num_sms, cudaStream_t st, int *launches, int cpx,
                            BatchMap vm = BatchMap());
@@ -96,6 +118,7 @@ struct GemmArgs {
     void *out;               // EPI_LEVELS_I64: int64 [s][n][m];  EPI_PAIR_I32: int32 [n][m]
     int64_t *chunk_scratch;  // per-CTA partial level sums when k_chunks > 1
     unsigned int *wave_counter;  // 4-byte device scratch for the soft wave barrier (or null)
+    bool counter_zeroed;         // wave_counter already zeroed on the stream (by k_split_small)
     long long *stats;            // optional per-CTA stall counters (development) or null
 };
 

@@ -16,6 +16,7 @@
 // transposing slice pass), write s B/element.  128-bit loads, 64-bit stores.
 #include <cstdint>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -431,6 +432,85 @@ __device__ __forceinline__ void contig_chunk(const double *v, int64_t l0, int64_
 // TPR threads per vector, one pass for the exponent (max reduction), one pass for
 // the digits (the second read of a <= 128 KB row hits L2).
 // ---------------------------------------------------------------------------------
+// One group of VPB = 256 / TPR contiguous vectors (rb-th group): pass 1 (exponent) and pass 2
+// (digits).  Called by every thread of the block (block-uniform rb); red: 8 ints of shared memory.
+template <int TPR, int W, int S, int CPX>
+__device__ __forceinline__ void contig_group(const double *__restrict__ M, int64_t ld, int64_t rows,
+                                             int64_t kdim, int64_t k_pad, int s, int reverse,
+                                             int conj, int8_t *__restrict__ planes,
+                                             int64_t plane_stride, int32_t *__restrict__ E,
+                                             int64_t per_item, int64_t item_stride, int64_t rb,
+                                             int32_t *red, uint64_t keep, uint64_t strm, bool use) {
+    constexpr int VPB = 256 / TPR;  // vectors per block
+    const int sub = threadIdx.x / TPR;
+    const int t = threadIdx.x % TPR;
+    const int64_t nchunk = k_pad / 8;
+    const int64_t r = rb * VPB + sub;
+    const bool active = r < rows;
+    const double *v = M + vec_off(active ? r : 0, ld, per_item, item_stride);
+    const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
+
+    // ---- pass 1: E = max exponent key ----
+    int32_t key = kKeyEmpty;
+    if (active) {
+        // four chunks' loads in flight per thread (memory parallelism with few blocks per
+        // SM, which keeps the vectors in flight -- and so pass 2's re-reads -- in L2); the
+        // max of the high words |x|_hi decides E unless everything is subnormal or zero
+        uint32_t mx = 0;
+        int64_t c = t;
+        for (; c + 3 * TPR < nchunk; c += 4 * TPR) {
+            double x[4][8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) load8(v, (c + u * TPR) * 8, kdim, al16, x[u], keep, use);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[u][i]));
+        }
+        for (; c < nchunk; c += TPR) {
+            double x[8];
+            load8(v, c * 8, kdim, al16, x, keep, use);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[i]));
+        }
+        key = key_from_hi(mx, [&]() {  // this thread saw only subnormals / zeros: exact
+            int32_t k2 = kKeyEmpty;
+            for (int64_t c2 = t; c2 < nchunk; c2 += TPR) {
+                double x[8];
+                load8(v, c2 * 8, kdim, al16, x);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) k2 = max(k2, exp_key(x[i]));
+            }
+            return k2;
+        });
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
+    if (TPR > 32) {
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
+        __syncthreads();
+        key = red[0];
+#pragma unroll
+        for (int i = 1; i < TPR / 32; ++i) key = max(key, red[i]);
+        __syncthreads();  // red[] is rewritten by the next vector
+    }
+    if (!active) return;
+    const int32_t Ev = key_to_exp(key);
+    if (t == 0) {
+        if (CPX == 2) {
+            E[2 * r] = Ev;
+            E[2 * r + 1] = Ev;
+        } else {
+            E[r] = Ev;
+        }
+    }
+
+    // ---- pass 2: digits ----
+    for (int64_t c = t; c < nchunk; c += TPR)
+        contig_chunk<W, S, CPX>(v, c * 8, kdim, al16, Ev, s, reverse, conj, planes, r, k_pad,
+                                plane_stride, strm, strm, use);
+}
+
 template <int TPR, int W, int S, int CPX>
 __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__ M, int64_t ld,
                                                       int64_t rows, int64_t kdim, int64_t k_pad,
@@ -445,78 +525,13 @@ __global__ void __launch_bounds__(256) k_split_contig(const double *__restrict__
     const bool use = hints != 0;
     const uint64_t keep = use ? l2_policy(HINT_KEEP) : 0, strm = use ? l2_policy(HINT_STREAM) : 0;
     __shared__ int32_t red[256 / 32];
-    const int sub = threadIdx.x / TPR;
-    const int t = threadIdx.x % TPR;
-    const int64_t nchunk = k_pad / 8;
     // Persistent blocks (grid sized by the host to a few blocks per SM): the vectors in
     // flight (grid x VPB x 8 k bytes) stay well inside L2, so pass 2 re-reads a vector from
     // L2 instead of HBM.
-    for (int64_t rb = blockIdx.x; rb * VPB < rows; rb += gridDim.x) {
-        const int64_t r = rb * VPB + sub;
-        const bool active = r < rows;
-        const double *v = M + vec_off(active ? r : 0, ld, per_item, item_stride);
-        const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
-
-        // ---- pass 1: E = max exponent key ----
-        int32_t key = kKeyEmpty;
-        if (active) {
-            // four chunks' loads in flight per thread (memory parallelism with few blocks per
-            // SM, which keeps the vectors in flight -- and so pass 2's re-reads -- in L2); the
-            // max of the high words |x|_hi decides E unless everything is subnormal or zero
-            uint32_t mx = 0;
-            int64_t c = t;
-            for (; c + 3 * TPR < nchunk; c += 4 * TPR) {
-                double x[4][8];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) load8(v, (c + u * TPR) * 8, kdim, al16, x[u], keep, use);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[u][i]));
-            }
-            for (; c < nchunk; c += TPR) {
-                double x[8];
-                load8(v, c * 8, kdim, al16, x, keep, use);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[i]));
-            }
-            key = key_from_hi(mx, [&]() {  // this thread saw only subnormals / zeros: exact
-                int32_t k2 = kKeyEmpty;
-                for (int64_t c2 = t; c2 < nchunk; c2 += TPR) {
-                    double x[8];
-                    load8(v, c2 * 8, kdim, al16, x);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) k2 = max(k2, exp_key(x[i]));
-                }
-                return k2;
-            });
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o));
-        if (TPR > 32) {
-            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = key;
-            __syncthreads();
-            key = red[0];
-#pragma unroll
-            for (int i = 1; i < TPR / 32; ++i) key = max(key, red[i]);
-            __syncthreads();  // red[] is rewritten by the next vector
-        }
-        if (!active) continue;
-        const int32_t Ev = key_to_exp(key);
-        if (t == 0) {
-            if (CPX == 2) {
-                E[2 * r] = Ev;
-                E[2 * r + 1] = Ev;
-            } else {
-                E[r] = Ev;
-            }
-        }
-
-        // ---- pass 2: digits ----
-        for (int64_t c = t; c < nchunk; c += TPR)
-            contig_chunk<W, S, CPX>(v, c * 8, kdim, al16, Ev, s, reverse, conj, planes, r, k_pad,
-                                    plane_stride, strm, strm, use);
-    }
+    for (int64_t rb = blockIdx.x; rb * VPB < rows; rb += gridDim.x)
+        contig_group<TPR, W, S, CPX>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes,
+                                     plane_stride, E, per_item, item_stride, rb, red, keep, strm,
+                                     use);
 }
 
 // ---------------------------------------------------------------------------------
@@ -689,6 +704,108 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
     }
     strided_tile<W, S, CPX>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride,
                             per_item, item_stride, r0, l0, tile, exps);
+}
+
+// ---------------------------------------------------------------------------------
+// Large strided operands, panel by panel (op(A) with transA = N at 16384^2: 2.1 GB, 17x L2):
+// launch j runs the exponent scan of row panel j (reads from HBM, kept in L2 with evict_last)
+// AND the digits of panel j-1 (scanned by the previous launch, so read from L2, evict_first;
+// planes streamed out), so HBM sees each element once: (8 + s) B per element instead of
+// (16 + s) for the scan-then-slice pair over the whole operand.  Block ranges: the first
+// `nscan` blocks scan (one thread per vector over lchunk elements, atomicMax into keys, as
+// k_expscan_strided), the rest are 32 x 128 slice tiles (as k_split_strided).
+// ---------------------------------------------------------------------------------
+template <int W, int S>
+__global__ void __launch_bounds__(256) k_split_strided_panel(
+    const double *__restrict__ M, int64_t ld, int64_t rows, int64_t kdim, int64_t k_pad, int s,
+    int reverse, int32_t *__restrict__ keys, int8_t *__restrict__ planes, int64_t plane_stride,
+    int32_t *__restrict__ E, int64_t per_item, int64_t item_stride, int64_t scan_r0,
+    int64_t scan_r1, int64_t lchunk, int64_t ysplit, int64_t slice_r0, int64_t slice_r1,
+    int hints) {
+    __shared__ __align__(16) double tile[32][128];  // [r][swizzled l]
+    __shared__ int32_t exps[32];
+    const bool use = hints != 0;
+    const int64_t rblocks = (scan_r1 - scan_r0 + 255) / 256;
+    const int64_t nscan = rblocks * ysplit;
+    const int tid = threadIdx.x;
+    if ((int64_t)blockIdx.x < nscan) {
+        const uint64_t keep = use ? l2_policy(HINT_KEEP) : 0;
+        const int64_t rb = blockIdx.x % rblocks, y = blockIdx.x / rblocks;
+        const int64_t r = scan_r0 + rb * 256 + tid;
+        if (r >= scan_r1) return;
+        const int64_t ro = vec_off(r, 1, per_item, item_stride);
+        const int64_t l0 = y * lchunk;
+        const int64_t l1 = min(kdim, l0 + lchunk);
+        uint32_t mx = 0;
+        int32_t key = kKeyEmpty;
+        int64_t l = l0;
+        for (; l + 8 <= l1; l += 8) {
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = ldg1_hint(M + ro + (l + i) * ld, keep, use);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[i]));
+            if (mx < 0x00100000u) {  // only subnormals / zeros so far: exact keys
+#pragma unroll
+                for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
+            }
+        }
+        for (; l < l1; ++l) {
+            const double x = ldg1_hint(M + ro + l * ld, keep, use);
+            mx = max(mx, abs_hi(x));
+            key = max(key, exp_key(x));
+        }
+        key = key_from_hi(mx, [&]() { return key; });
+        if (key != kKeyEmpty) atomicMax(keys + r, key);
+        return;
+    }
+    const uint64_t strm = use ? l2_policy(HINT_STREAM) : 0;
+    const int64_t nlb = (k_pad + 127) / 128;
+    const int64_t t = blockIdx.x - nscan;
+    const int64_t rg = t / nlb;
+    const int64_t r0 = slice_r0 + rg * 32, l0 = (t - rg * nlb) * 128;
+    if (tid < 32) {
+        const int64_t r = r0 + tid;
+        int32_t e = 0;
+        if (r < slice_r1) {
+            e = key_to_exp(__ldcg(keys + r));
+            if (l0 == 0) E[r] = e;
+        }
+        exps[tid] = e;
+    }
+    strided_tile<W, S, 0>(M, ld, slice_r1, kdim, k_pad, s, reverse, 0, planes, plane_stride,
+                          per_item, item_stride, r0, l0, tile, exps, strm, use);
+}
+
+int split_hints();
+
+template <int W, int S>
+cudaError_t launch_strided_panels(const double *M, int64_t ld, int64_t rows, int64_t kdim,
+                                  int64_t k_pad, int s, bool reverse, int8_t *planes,
+                                  int64_t plane_stride, int32_t *E, int32_t *keys, int64_t PR,
+                                  int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
+    cudaError_t e = cudaMemsetAsync(keys, 0x80, sizeof(int32_t) * rows, st);
+    if (e != cudaSuccess) return e;
+    // scan split: >= ~4 blocks per SM over a panel's vectors, >= 64 elements per thread
+    const int64_t rblocks = ceil_div(PR, 256);
+    int64_t lchunk = round_up(ceil_div(kdim * rblocks, 4 * (int64_t)num_sms), 8);
+    if (lchunk < 64) lchunk = 64;
+    const int64_t ysplit = ceil_div(kdim, lchunk);
+    const int64_t NP = ceil_div(rows, PR);
+    const int64_t nlb = ceil_div(k_pad, 128);
+    for (int64_t j = 0; j <= NP; ++j) {
+        const int64_t sr0 = j < NP ? j * PR : 0, sr1 = j < NP ? min(rows, (j + 1) * PR) : 0;
+        const int64_t cr0 = j > 0 ? (j - 1) * PR : 0, cr1 = j > 0 ? min(rows, j * PR) : 0;
+        const int64_t nscan = sr1 > sr0 ? ceil_div(sr1 - sr0, 256) * ysplit : 0;
+        const int64_t nslice = cr1 > cr0 ? ceil_div(cr1 - cr0, 32) * nlb : 0;
+        k_split_strided_panel<W, S><<<(unsigned)(nscan + nslice), 256, 0, st>>>(
+            M, ld, rows, kdim, k_pad, s, reverse, keys, planes, plane_stride, E, vm.per_item,
+            vm.stride, sr0, sr1 > sr0 ? sr1 : sr0, lchunk, ysplit, cr0, cr1, split_hints());
+        ++*launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------------
@@ -932,6 +1049,258 @@ __global__ void __launch_bounds__(256, (W * S <= 96) ? OZ_FUSED_MINB : 1) k_spli
     }
 }
 
+// ---------------------------------------------------------------------------------
+// Small calls (both operands together fit comfortably in L2): op(A) AND op(B) sliced in ONE
+// cooperative launch instead of 3-4 launches on two streams (exponent-key memset, scan, slice
+// on one stream, the other operand on the second, event fork / join) -- at 1024^3-2048^3 the
+// slicing phase is launch- and latency-bound, not HBM-bound.
+//  phase 1: exponent-scan tiles of both operands -- strided: 32 vectors x 512 elements (a warp
+//           reads 32 consecutive vectors at one l); contiguous: 8 vectors x 512 elements (a
+//           warp per vector) -- each writing its partial key part[ly * rows + r] (ly = l / 512),
+//           so nothing needs initialising and no atomics are used;
+//  grid-wide barrier;
+//  phase 2: digit tiles -- strided: the transposing 32 x 128 tile (strided_tile); contiguous:
+//           8 vectors x 512 elements, both 8-element chunks of a lane loaded before either is
+//           converted -- with E = max of the vector's partial keys.
+// Element arithmetic is that of the per-operand kernels (same device functions), so planes and
+// exponents are bit-identical.  Block 0 also zeroes the GEMM's wave counter, which saves the
+// GEMM launch its memset.
+// ---------------------------------------------------------------------------------
+// partial keys per vector: one per 512 elements (contiguous) / 128 elements (strided)
+__host__ __device__ __forceinline__ int64_t small_nls(const SmallOp &o) {
+    return o.contig ? (o.kdim + 511) / 512 : (o.kdim + 127) / 128;
+}
+__host__ __device__ __forceinline__ int64_t small_items1(const SmallOp &o) {
+    if (o.rows <= 0) return 0;
+    return (o.contig ? (o.rows + 7) / 8 : (o.rows + 31) / 32) * small_nls(o);
+}
+__host__ __device__ __forceinline__ int64_t small_items2(const SmallOp &o) {
+    if (o.rows <= 0) return 0;
+    if (o.contig) return ((o.rows + 7) / 8) * ((o.k_pad + 255) / 256);
+    return ((o.rows + 31) / 32) * ((o.k_pad + 127) / 128);
+}
+
+// Partial exponent keys of 32 strided vectors over 512 elements (tile t of operand o).
+__device__ __forceinline__ void small_scan_strided(const SmallOp &o, int64_t t, int32_t (*red)[32]) {
+    const int64_t nls = small_nls(o);
+    const int64_t rg = t / nls, ly = t - rg * nls;
+    const int64_t r0 = rg * 32, l0 = ly * 128;
+    const int tid = threadIdx.x, rr = tid & 31, lg = tid >> 5;
+    const int64_t r = r0 + rr;
+    int32_t key = kKeyEmpty;
+    if (r < o.rows) {
+        const int64_t ro = vec_off(r, 1, o.per_item, o.item_stride);
+        const double *q = o.M + ro + (l0 + lg) * o.ld;
+        const int64_t kl = o.kdim - (l0 + lg);  // elements left from this thread's first
+        const int64_t step = 8 * o.ld;
+        const bool full = kl > 8 * 15;
+        double x[16];
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {
+            x[it] = (full || 8 * it < kl) ? __ldg(q) : 0.0;
+            q += step;
+        }
+        uint32_t mx = 0;
+#pragma unroll
+        for (int it = 0; it < 16; ++it) mx = max(mx, abs_hi(x[it]));
+        key = key_from_hi(mx, [&]() {  // only subnormals / zeros: exact keys
+            int32_t k2 = kKeyEmpty;
+#pragma unroll
+            for (int it = 0; it < 16; ++it) k2 = max(k2, exp_key(x[it]));
+            return k2;
+        });
+    }
+    red[lg][rr] = key;
+    __syncthreads();
+    if (tid < 32) {
+#pragma unroll
+        for (int i = 1; i < 8; ++i) key = max(key, red[i][tid]);
+        if (r < o.rows) o.part[ly * o.rows + r] = key;
+    }
+    __syncthreads();  // red[] is rewritten by the next tile
+}
+
+// Partial exponent keys of 8 contiguous vectors over 512 elements: warp wv takes vector
+// r0 + wv, lane `lane` elements l0 + 16 lane .. + 15.
+__device__ __forceinline__ void small_scan_contig(const SmallOp &o, int64_t t) {
+    const int64_t nls = small_nls(o);
+    const int64_t rg = t / nls, ly = t - rg * nls;
+    const int lane = threadIdx.x & 31;
+    const int64_t r = rg * 8 + (threadIdx.x >> 5);
+    if (r >= o.rows) return;  // warp-uniform
+    const double *v = o.M + vec_off(r, o.ld, o.per_item, o.item_stride);
+    const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
+    const int64_t l = ly * 512 + 16 * lane;
+    double x0[8], x1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x0[i] = x1[i] = 0.0;
+    if (l < o.kdim) load8(v, l, o.kdim, al16, x0);
+    if (l + 8 < o.kdim) load8(v, l + 8, o.kdim, al16, x1);
+    uint32_t mx = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mx = max(mx, max(abs_hi(x0[i]), abs_hi(x1[i])));
+    int32_t key = key_from_hi(mx, [&]() {
+        int32_t k2 = kKeyEmpty;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) k2 = max(k2, max(exp_key(x0[i]), exp_key(x1[i])));
+        return k2;
+    });
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o2));
+    if (lane == 0) o.part[ly * o.rows + r] = key;
+}
+
+// E of vector r from its partial keys (whole warp; every lane gets it).
+__device__ __forceinline__ int32_t small_exp_warp(const SmallOp &o, int64_t r) {
+    const int64_t nls = small_nls(o);
+    int32_t key = kKeyEmpty;
+    for (int64_t y = threadIdx.x & 31; y < nls; y += 32) key = max(key, __ldcg(o.part + y * o.rows + r));
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o2));
+    return key_to_exp(key);
+}
+
+// Digits of 8 loaded elements (x is clobbered), as contig_chunk / strided_tile compute them.
+template <int W, int S>
+__device__ __forceinline__ void small_digits8(double (&x)[8], int32_t Ev, int s, int reverse,
+                                              int8_t *planes, int64_t r, int64_t lb, int64_t k_pad,
+                                              int64_t plane_stride) {
+    const bool bad = Ev == kExpNonFinite;
+    if constexpr (W * S <= 96) {
+        if (bad) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = 0.0;
+        }
+        Chunk64<W, S> c;
+        c.init(x, bad ? 0 : Ev);
+        emit64<W, S, 0>(c, s, reverse, 0, planes, r, lb, k_pad, plane_stride, 0, false);
+    } else {
+        Digits<W, S> dg[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
+        emit<W, S, 0>(dg, s, reverse, 0, planes, r, lb, k_pad, plane_stride);
+    }
+}
+
+// Digits of 8 contiguous vectors x 256 elements (warp per vector, lane: the chunk at l0 + 8 lane,
+// i.e. 256-byte coalesced warp loads).
+template <int W, int S>
+__device__ __forceinline__ void small_digits_contig(const SmallOp &o, int64_t t, int s) {
+    const int64_t nlb = (o.k_pad + 255) / 256;
+    const int64_t rg = t / nlb, lb = t - rg * nlb;
+    const int lane = threadIdx.x & 31;
+    const int64_t r = rg * 8 + (threadIdx.x >> 5);
+    if (r >= o.rows) return;  // warp-uniform
+    const int64_t l0 = lb * 256 + 8 * lane;
+    const double *v = o.M + vec_off(r, o.ld, o.per_item, o.item_stride);
+    const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
+    double x[8];
+    if (l0 < o.kdim) load8(v, l0, o.kdim, al16, x);  // issued before the exponent's reduction
+    const int32_t Ev = small_exp_warp(o, r);
+    if (lb == 0 && lane == 0) o.E[r] = Ev;
+    if (l0 >= o.k_pad) return;
+    if (l0 >= o.kdim) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = 0.0;
+    }
+    small_digits8<W, S>(x, Ev, s, o.reverse, o.planes, r, l0, o.k_pad, o.plane_stride);
+}
+
+template <int W, int S>
+__device__ __forceinline__ void small_digits_strided(const SmallOp &o, int64_t t, int s,
+                                                     double (*tile)[128], int32_t *exps,
+                                                     int32_t (*red)[32]) {
+    const int64_t nlb = (o.k_pad + 127) / 128, nls = small_nls(o);
+    const int64_t rg = t / nlb;
+    const int64_t r0 = rg * 32, l0 = (t - rg * nlb) * 128;
+    const int tid = threadIdx.x;
+    {  // E of the tile's 32 vectors: 8 warps reduce the partial keys, then one warp combines
+        const int rr = tid & 31, yg = tid >> 5;
+        const int64_t r = r0 + rr;
+        int32_t key = kKeyEmpty;
+        if (r < o.rows)
+            for (int64_t y = yg; y < nls; y += 8) key = max(key, __ldcg(o.part + y * o.rows + r));
+        red[yg][rr] = key;
+    }
+    __syncthreads();
+    if (tid < 32) {
+        const int64_t r = r0 + tid;
+        int32_t key = red[0][tid];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) key = max(key, red[i][tid]);
+        const int32_t e = r < o.rows ? key_to_exp(key) : 0;
+        if (r < o.rows && l0 == 0) o.E[r] = e;
+        exps[tid] = e;
+    }
+    strided_tile<W, S, 0>(o.M, o.ld, o.rows, o.kdim, o.k_pad, s, o.reverse, 0, o.planes,
+                          o.plane_stride, o.per_item, o.item_stride, r0, l0, tile, exps);
+    __syncthreads();  // tile / exps are rewritten by the next tile
+}
+
+template <int W, int S>
+__global__ void __launch_bounds__(256, (S <= 13) ? 3 : 1) k_split_small(const __grid_constant__ SmallOp a,
+                                                     const __grid_constant__ SmallOp b, int s,
+                                                     unsigned int *zero_ctr) {
+    __shared__ __align__(16) double tile[32][128];
+    __shared__ int32_t red[8][32];
+    __shared__ int32_t exps[32];
+    if (zero_ctr && blockIdx.x == 0 && threadIdx.x == 0) *zero_ctr = 0u;
+    const int64_t na = small_items1(a), nb = small_items1(b);
+    for (int64_t i = blockIdx.x; i < na + nb; i += gridDim.x) {
+        const bool ia = i < na;
+        const SmallOp &o = *(ia ? &a : &b);  // stays in the parameter space (__grid_constant__)
+        const int64_t t = ia ? i : i - na;
+        if (o.contig) small_scan_contig(o, t);
+        else small_scan_strided(o, t, red);
+    }
+    cooperative_groups::this_grid().sync();  // every partial key written and visible
+    // the GEMM (launched with programmatic stream serialisation) may start its set-up on SMs
+    // this grid leaves; it waits for this grid's completion before reading the planes
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int64_t ma = small_items2(a), mb = small_items2(b);
+    for (int64_t i = blockIdx.x; i < ma + mb; i += gridDim.x) {
+        const bool ia = i < ma;
+        const SmallOp &o = *(ia ? &a : &b);
+        const int64_t t = ia ? i : i - ma;
+        if (o.contig) small_digits_contig<W, S>(o, t, s);
+        else small_digits_strided<W, S>(o, t, s, tile, exps, red);
+    }
+}
+
+template <int W, int S>
+cudaError_t launch_small_t(const SmallOp &a, const SmallOp &b, int s, unsigned int *zero_ctr,
+                           int num_sms, cudaStream_t st) {
+    auto kern = k_split_small<W, S>;
+    static int occ = 0;  // resident blocks per SM (per instantiation; same on every B200)
+    if (occ == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0) != cudaSuccess ||
+            occ < 1) {
+            cudaGetLastError();
+            occ = 0;
+            return cudaErrorInvalidConfiguration;
+        }
+    }
+    const int64_t n1 = small_items1(a) + small_items1(b);
+    const int64_t n2 = small_items2(a) + small_items2(b);
+    const int64_t need = n1 > n2 ? n1 : n2;
+    const int64_t cap = (int64_t)occ * num_sms;
+    const unsigned grid = (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
+    SmallOp a_ = a, b_ = b;
+    int s_ = s;
+    unsigned int *z_ = zero_ctr;
+    void *args[] = {&a_, &b_, &s_, &z_};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st);
+}
+
+template <int W>
+cudaError_t launch_small_w(const SmallOp &a, const SmallOp &b, int s, unsigned int *zero_ctr,
+                           int num_sms, cudaStream_t st) {
+    if (s <= 9) return launch_small_t<W, 9>(a, b, s, zero_ctr, num_sms, st);
+    if (s <= 13) return launch_small_t<W, 13>(a, b, s, zero_ctr, num_sms, st);
+    if (s <= 16) return launch_small_t<W, 16>(a, b, s, zero_ctr, num_sms, st);
+    return launch_small_t<W, 32>(a, b, s, zero_ctr, num_sms, st);
+}
+
 }  // namespace
 
 // Exponent keys of strided vectors (element l of vector r at M[r + l ld]; cpx: (re, im)
@@ -1060,6 +1429,21 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
     if (fused) return launch_fused<W, S, CPX, false>(M, ld, rows, kdim, k_pad, s, reverse, conj,
                                                       planes, plane_stride, E, key_scratch,
                                                       num_sms, st, launches, vm);
+    // large real operands: panel-pipelined scan + slice (k_split_strided_panel), panels of
+    // ~OZIMMU_SPLIT_PANEL_MB (default 32) of input, a multiple of 256 vectors
+    if constexpr (CPX == 0) {
+        static const int64_t pmb =
+            getenv("OZIMMU_SPLIT_PANEL_MB") ? atoi(getenv("OZIMMU_SPLIT_PANEL_MB")) : 32;
+        const int64_t bytes = rows * kdim * 8;
+        if (pmb > 0 && bytes > 4 * (pmb << 20)) {
+            int64_t PR = ((pmb << 20) / (kdim * 8)) / 256 * 256;
+            if (PR < 256) PR = 256;
+            if (PR < rows)
+                return launch_strided_panels<W, S>(M, ld, rows, kdim, k_pad, s, reverse, planes,
+                                                   plane_stride, E, key_scratch, PR, num_sms, st,
+                                                   launches, vm);
+        }
+    }
     cudaError_t e = launch_expscan(M, ld, rows, CPX ? kdim / 2 : kdim, key_scratch, num_sms, st,
                                    launches, CPX ? 1 : 0, vm);
     if (e != cudaSuccess) return e;
@@ -1129,6 +1513,40 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
                                      planes, plane_stride, E, key_scratch, num_sms, st, launches, vm);
     default: return cudaErrorInvalidValue;
     }
+}
+
+// Both operands of a small call in one launch (see k_split_small).
+size_t split_small_part_bytes(int64_t m, int64_t n, int64_t k_pad) {
+    if (!split_small_ok(m, n, k_pad)) return 0;
+    // one partial key per 128 elements (strided) or 512 (contiguous) of each vector
+    return sizeof(int32_t) * (size_t)((k_pad + 127) / 128) * (size_t)(m + n);
+}
+
+bool split_small_ok(int64_t m, int64_t n, int64_t k_pad) {
+    // sum of both operands' input bytes <= OZIMMU_SPLIT_SMALL_MB.  Off by default (0): measured
+    // slower than the per-operand kernels on two streams (1024^3 slicing 21 -> 25
+    // us, 2048^3 45 -> 62 us) -- with ~3 resident blocks per SM each block walks its work items
+    // in rounds of dependent memory round trips, where the per-operand launches have every item
+    // in flight at once
+    static const int64_t lim =
+        (int64_t)(getenv("OZIMMU_SPLIT_SMALL_MB") ? atoi(getenv("OZIMMU_SPLIT_SMALL_MB")) : 0)
+        << 20;
+    return m > 0 && n > 0 && (m + n) * k_pad * 8 <= lim;
+}
+
+cudaError_t launch_split_small(const SmallOp &a, const SmallOp &b, int s, int w,
+                               unsigned int *zero_ctr, int num_sms, cudaStream_t st,
+                               int *launches) {
+    if (s < 1 || s > 32) return cudaErrorInvalidValue;
+    cudaError_t e;
+    switch (w) {
+    case 7: e = launch_small_w<7>(a, b, s, zero_ctr, num_sms, st); break;
+    case 6: e = launch_small_w<6>(a, b, s, zero_ctr, num_sms, st); break;
+    case 5: e = launch_small_w<5>(a, b, s, zero_ctr, num_sms, st); break;
+    default: return cudaErrorInvalidValue;
+    }
+    ++*launches;
+    return e;
 }
 
 }  // namespace ozimmu

@@ -16,12 +16,18 @@ SPLITS = [("N", 1, 300, 1000, 9), ("T", 1, 300, 3000, 9), ("N", 0, 77, 2100, 13)
           ("T", 1, 33, 20000, 9), ("N", 0, 5, 4096, 20), ("T", 0, 257, 128, 5),
           # 96-bit fraction window of the fast digit path (10 <= s <= 13 at w = 7)
           ("N", 1, 70, 700, 10), ("T", 1, 45, 2500, 11), ("N", 0, 90, 3000, 12),
-          ("T", 0, 64, 300, 13)]
+          ("T", 0, 64, 300, 13),
+          # strided operands of > 4 panels at OZIMMU_SPLIT_PANEL_MB=1 (ragged last panel)
+          ("N", 1, 1100, 1500, 9), ("T", 0, 700, 3000, 13)]
 # dgemm: (ta, tb, m, n, k, s)
 DGEMMS = [("N", "N", 300, 200, 5000, 9), ("T", "T", 129, 300, 2500, 13),
           ("N", "T", 64, 70, 20000, 9), ("T", "N", 1, 2049, 2048, 7),
           # short K, s <= 8: two TMEM accumulator buffers (N_c = 32 / default width)
-          ("N", "N", 1000, 300, 1000, 8), ("T", "N", 257, 129, 64, 4), ("N", "T", 600, 97, 300, 3)]
+          ("N", "N", 1000, 300, 1000, 8), ("T", "N", 257, 129, 64, 4), ("N", "T", 600, 97, 300, 3),
+          # k > 2^17: w = 6 digits
+          ("N", "T", 24, 40, 140000, 9),
+          # op(A) strided over several 1 MB panels
+          ("N", "N", 1300, 64, 1200, 9)]
 # zgemm: (ta, tb, m, n, k, s)
 ZGEMMS = [("N", "N", 200, 96, 1500, 9), ("C", "T", 70, 45, 1100, 12), ("T", "C", 65, 33, 2100, 8),
           ("N", "T", 3000, 64, 256, 8)]

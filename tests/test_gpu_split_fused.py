@@ -2,7 +2,9 @@
 panel in one persistent launch, slice tiles waiting on their panel's scan tiles; SplitInt,
 Alg. 4, readings A3-A5/A11).  Children run with the fused kernel at its default
 panel size, with tiny panels (many panels, ragged last panel, scans and slices of different
-panels interleaved) and with the two-launch path (OZIMMU_SPLIT_FUSED=0); the GEMM cases also
+panels interleaved) and with the two-launch path (OZIMMU_SPLIT_FUSED=0); the DGEMMs also run
+with both operands sliced in one cooperative launch (k_split_small, OZIMMU_SPLIT_SMALL_MB); the
+GEMM cases also
 run with one TMEM accumulator instead of two (OZIMMU_ACC2=0).  Planes, exponents and C must
 be bitwise equal across the variants and to the CPU oracle."""
 import os
@@ -25,6 +27,12 @@ VARIANTS = {"two_launch": {"OZIMMU_SPLIT_FUSED": "0"},
             "fused": {"OZIMMU_SPLIT_FUSED": "1"},
             "fused_small_panels": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_PANEL_KB": "24"},
             "fused_bps2": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_FUSED_BPS": "2"},
+            # both operands of a DGEMM in one cooperative launch (k_split_small, opt-in)
+            "small_one_launch": {"OZIMMU_SPLIT_SMALL_MB": "512"},
+            # large strided operands panel by panel (k_split_strided_panel), 1 MB panels so
+            # that the cases below take several panels with a ragged last one; and disabled
+            "strided_panels": {"OZIMMU_SPLIT_PANEL_MB": "1"},
+            "no_panels": {"OZIMMU_SPLIT_PANEL_MB": "0"},
             # GEMM side: one TMEM accumulator buffer instead of two for short K (s <= 8)
             "one_acc": {"OZIMMU_ACC2": "0"}}
 
