@@ -707,108 +707,6 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
 }
 
 // ---------------------------------------------------------------------------------
-// Large strided operands, panel by panel (op(A) with transA = N at 16384^2: 2.1 GB, 17x L2):
-// launch j runs the exponent scan of row panel j (reads from HBM, kept in L2 with evict_last)
-// AND the digits of panel j-1 (scanned by the previous launch, so read from L2, evict_first;
-// planes streamed out), so HBM sees each element once: (8 + s) B per element instead of
-// (16 + s) for the scan-then-slice pair over the whole operand.  Block ranges: the first
-// `nscan` blocks scan (one thread per vector over lchunk elements, atomicMax into keys, as
-// k_expscan_strided), the rest are 32 x 128 slice tiles (as k_split_strided).
-// ---------------------------------------------------------------------------------
-template <int W, int S>
-__global__ void __launch_bounds__(256) k_split_strided_panel(
-    const double *__restrict__ M, int64_t ld, int64_t rows, int64_t kdim, int64_t k_pad, int s,
-    int reverse, int32_t *__restrict__ keys, int8_t *__restrict__ planes, int64_t plane_stride,
-    int32_t *__restrict__ E, int64_t per_item, int64_t item_stride, int64_t scan_r0,
-    int64_t scan_r1, int64_t lchunk, int64_t ysplit, int64_t slice_r0, int64_t slice_r1,
-    int hints) {
-    __shared__ __align__(16) double tile[32][128];  // [r][swizzled l]
-    __shared__ int32_t exps[32];
-    const bool use = hints != 0;
-    const int64_t rblocks = (scan_r1 - scan_r0 + 255) / 256;
-    const int64_t nscan = rblocks * ysplit;
-    const int tid = threadIdx.x;
-    if ((int64_t)blockIdx.x < nscan) {
-        const uint64_t keep = use ? l2_policy(HINT_KEEP) : 0;
-        const int64_t rb = blockIdx.x % rblocks, y = blockIdx.x / rblocks;
-        const int64_t r = scan_r0 + rb * 256 + tid;
-        if (r >= scan_r1) return;
-        const int64_t ro = vec_off(r, 1, per_item, item_stride);
-        const int64_t l0 = y * lchunk;
-        const int64_t l1 = min(kdim, l0 + lchunk);
-        uint32_t mx = 0;
-        int32_t key = kKeyEmpty;
-        int64_t l = l0;
-        for (; l + 8 <= l1; l += 8) {
-            double x[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = ldg1_hint(M + ro + (l + i) * ld, keep, use);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) mx = max(mx, abs_hi(x[i]));
-            if (mx < 0x00100000u) {  // only subnormals / zeros so far: exact keys
-#pragma unroll
-                for (int i = 0; i < 8; ++i) key = max(key, exp_key(x[i]));
-            }
-        }
-        for (; l < l1; ++l) {
-            const double x = ldg1_hint(M + ro + l * ld, keep, use);
-            mx = max(mx, abs_hi(x));
-            key = max(key, exp_key(x));
-        }
-        key = key_from_hi(mx, [&]() { return key; });
-        if (key != kKeyEmpty) atomicMax(keys + r, key);
-        return;
-    }
-    const uint64_t strm = use ? l2_policy(HINT_STREAM) : 0;
-    const int64_t nlb = (k_pad + 127) / 128;
-    const int64_t t = blockIdx.x - nscan;
-    const int64_t rg = t / nlb;
-    const int64_t r0 = slice_r0 + rg * 32, l0 = (t - rg * nlb) * 128;
-    if (tid < 32) {
-        const int64_t r = r0 + tid;
-        int32_t e = 0;
-        if (r < slice_r1) {
-            e = key_to_exp(__ldcg(keys + r));
-            if (l0 == 0) E[r] = e;
-        }
-        exps[tid] = e;
-    }
-    strided_tile<W, S, 0>(M, ld, slice_r1, kdim, k_pad, s, reverse, 0, planes, plane_stride,
-                          per_item, item_stride, r0, l0, tile, exps, strm, use);
-}
-
-int split_hints();
-
-template <int W, int S>
-cudaError_t launch_strided_panels(const double *M, int64_t ld, int64_t rows, int64_t kdim,
-                                  int64_t k_pad, int s, bool reverse, int8_t *planes,
-                                  int64_t plane_stride, int32_t *E, int32_t *keys, int64_t PR,
-                                  int num_sms, cudaStream_t st, int *launches, BatchMap vm) {
-    cudaError_t e = cudaMemsetAsync(keys, 0x80, sizeof(int32_t) * rows, st);
-    if (e != cudaSuccess) return e;
-    // scan split: >= ~4 blocks per SM over a panel's vectors, >= 64 elements per thread
-    const int64_t rblocks = ceil_div(PR, 256);
-    int64_t lchunk = round_up(ceil_div(kdim * rblocks, 4 * (int64_t)num_sms), 8);
-    if (lchunk < 64) lchunk = 64;
-    const int64_t ysplit = ceil_div(kdim, lchunk);
-    const int64_t NP = ceil_div(rows, PR);
-    const int64_t nlb = ceil_div(k_pad, 128);
-    for (int64_t j = 0; j <= NP; ++j) {
-        const int64_t sr0 = j < NP ? j * PR : 0, sr1 = j < NP ? min(rows, (j + 1) * PR) : 0;
-        const int64_t cr0 = j > 0 ? (j - 1) * PR : 0, cr1 = j > 0 ? min(rows, j * PR) : 0;
-        const int64_t nscan = sr1 > sr0 ? ceil_div(sr1 - sr0, 256) * ysplit : 0;
-        const int64_t nslice = cr1 > cr0 ? ceil_div(cr1 - cr0, 32) * nlb : 0;
-        k_split_strided_panel<W, S><<<(unsigned)(nscan + nslice), 256, 0, st>>>(
-            M, ld, rows, kdim, k_pad, s, reverse, keys, planes, plane_stride, E, vm.per_item,
-            vm.stride, sr0, sr1 > sr0 ? sr1 : sr0, lchunk, ysplit, cr0, cr1, split_hints());
-        ++*launches;
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-}
-
-// ---------------------------------------------------------------------------------
 // One read of the operand from HBM (large operands): exponent scan and digits in ONE
 // persistent launch.  The vectors are grouped in panels of ~16 MB of input; the work items
 // are, in this order, the scan tiles of panel 0, then for q = 1 .. NP-1 the scan tiles of
@@ -1429,21 +1327,6 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
     if (fused) return launch_fused<W, S, CPX, false>(M, ld, rows, kdim, k_pad, s, reverse, conj,
                                                       planes, plane_stride, E, key_scratch,
                                                       num_sms, st, launches, vm);
-    // large real operands: panel-pipelined scan + slice (k_split_strided_panel), panels of
-    // ~OZIMMU_SPLIT_PANEL_MB (default 32) of input, a multiple of 256 vectors
-    if constexpr (CPX == 0) {
-        static const int64_t pmb =
-            getenv("OZIMMU_SPLIT_PANEL_MB") ? atoi(getenv("OZIMMU_SPLIT_PANEL_MB")) : 32;
-        const int64_t bytes = rows * kdim * 8;
-        if (pmb > 0 && bytes > 4 * (pmb << 20)) {
-            int64_t PR = ((pmb << 20) / (kdim * 8)) / 256 * 256;
-            if (PR < 256) PR = 256;
-            if (PR < rows)
-                return launch_strided_panels<W, S>(M, ld, rows, kdim, k_pad, s, reverse, planes,
-                                                   plane_stride, E, key_scratch, PR, num_sms, st,
-                                                   launches, vm);
-        }
-    }
     cudaError_t e = launch_expscan(M, ld, rows, CPX ? kdim / 2 : kdim, key_scratch, num_sms, st,
                                    launches, CPX ? 1 : 0, vm);
     if (e != cudaSuccess) return e;

@@ -17,7 +17,7 @@ SPLITS = [("N", 1, 300, 1000, 9), ("T", 1, 300, 3000, 9), ("N", 0, 77, 2100, 13)
           # 96-bit fraction window of the fast digit path (10 <= s <= 13 at w = 7)
           ("N", 1, 70, 700, 10), ("T", 1, 45, 2500, 11), ("N", 0, 90, 3000, 12),
           ("T", 0, 64, 300, 13),
-          # strided operands of > 4 panels at OZIMMU_SPLIT_PANEL_MB=1 (ragged last panel)
+          # larger strided operands (rows of op(A) with transA = N, columns of op(B) with T)
           ("N", 1, 1100, 1500, 9), ("T", 0, 700, 3000, 13)]
 # dgemm: (ta, tb, m, n, k, s)
 DGEMMS = [("N", "N", 300, 200, 5000, 9), ("T", "T", 129, 300, 2500, 13),
@@ -26,7 +26,7 @@ DGEMMS = [("N", "N", 300, 200, 5000, 9), ("T", "T", 129, 300, 2500, 13),
           ("N", "N", 1000, 300, 1000, 8), ("T", "N", 257, 129, 64, 4), ("N", "T", 600, 97, 300, 3),
           # k > 2^17: w = 6 digits
           ("N", "T", 24, 40, 140000, 9),
-          # op(A) strided over several 1 MB panels
+          # op(A) strided, ~1000 rows
           ("N", "N", 1300, 64, 1200, 9)]
 # zgemm: (ta, tb, m, n, k, s)
 ZGEMMS = [("N", "N", 200, 96, 1500, 9), ("C", "T", 70, 45, 1100, 12), ("T", "C", 65, 33, 2100, 8),

@@ -29,10 +29,6 @@ VARIANTS = {"two_launch": {"OZIMMU_SPLIT_FUSED": "0"},
             "fused_bps2": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_FUSED_BPS": "2"},
             # both operands of a DGEMM in one cooperative launch (k_split_small, opt-in)
             "small_one_launch": {"OZIMMU_SPLIT_SMALL_MB": "512"},
-            # large strided operands panel by panel (k_split_strided_panel), 1 MB panels so
-            # that the cases below take several panels with a ragged last one; and disabled
-            "strided_panels": {"OZIMMU_SPLIT_PANEL_MB": "1"},
-            "no_panels": {"OZIMMU_SPLIT_PANEL_MB": "0"},
             # GEMM side: one TMEM accumulator buffer instead of two for short K (s <= 8)
             "one_acc": {"OZIMMU_ACC2": "0"}}
 
