@@ -39,8 +39,6 @@ Layout layout(int64_t m, int64_t n, int64_t k_pad, int s, size_t scratch) {
     off += align_up(split_scratch_bytes(m > n ? m : n));
     L.keys_b = off;  // B's slicing scratch (B is sliced concurrently with A)
     off += align_up(split_scratch_bytes(n));
-    L.part = off;  // small calls: partial exponent keys of both operands (k_split_small)
-    off += align_up(split_small_part_bytes(m, n, k_pad));
     L.sync = off;
     off += kAlign;
     L.scratch = off;
@@ -390,13 +388,12 @@ ozimmu_status_t gemm_core(ozimmu_handle_t h, ozimmu_op_t transA, int64_t m, int6
     bool counter_zeroed = false;
     if (!bbuf_ext && split_small_ok(m, n, k_pad)) {
         uint8_t *b = base + L.b_buf;
-        int32_t *part = reinterpret_cast<int32_t *>(base + L.part);
-        SmallOp oa{A, lda, m, k, k_pad, transA != OZIMMU_OP_N, 0, a_planes, m * k_pad, EA, part,
+        SmallOp oa{A, lda, m, k, k_pad, transA != OZIMMU_OP_N, 0, a_planes, m * k_pad, EA,
                    amap.per_item, amap.stride};
         SmallOp ob{B, ldb, n, k, k_pad, transB == OZIMMU_OP_N, 1,
                    reinterpret_cast<int8_t *>(b), n * k_pad,
                    reinterpret_cast<int32_t *>(b + b_buf_planes_bytes(n, k_pad, s)),
-                   part + ((k_pad + 127) / 128) * m, bmap.per_item, bmap.stride};
+                   bmap.per_item, bmap.stride};
         mark(h, PH_B);
         cudaError_t e = launch_split_small(oa, ob, s, w, reinterpret_cast<unsigned int *>(base + L.sync),
                                            h->num_sms, h->stream, &launches);

@@ -63,7 +63,7 @@ inline int gemm_sms(ozimmu_handle_t h) {
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct Layout {  // workspace carve-up for one dgemm call
-    size_t a_planes, a_exp, b_buf, keys, keys_b, part, sync, scratch, total;
+    size_t a_planes, a_exp, b_buf, keys, keys_b, sync, scratch, total;
 };
 
 // Phase events of one computing call (ozimmu_timing_read): start, B sliced (on the stream

@@ -57,11 +57,9 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
                          BatchMap vm = BatchMap());
 
 // Small calls: both operands sliced in ONE launch (split.cu k_split_small; contiguous or
-// strided vectors, real operands; opt-in, measured slower).  part: the operands' partial
-// exponent keys, <= ceil(kdim / 128) x rows int32 each (no initialisation needed).
-// split_small_ok: the call is small enough (both operands' input bytes <=
-// OZIMMU_SPLIT_SMALL_MB, default 0 = off);
-// split_small_part_bytes: workspace for both operands' partials (0 when not small).
+// strided vectors, real operands), which also zeroes the GEMM's wave counter (zero_ctr).
+// split_small_ok: the call qualifies (both operands' input bytes <= OZIMMU_SPLIT_SMALL_MB,
+// default 80 MB, and k_pad <= 1024).
 struct SmallOp {
     const double *M;
     int64_t ld, rows, kdim, k_pad;
@@ -69,11 +67,9 @@ struct SmallOp {
     int8_t *planes;
     int64_t plane_stride;
     int32_t *E;
-    int32_t *part;
     int64_t per_item, item_stride;
 };
 bool split_small_ok(int64_t m, int64_t n, int64_t k_pad);
-size_t split_small_part_bytes(int64_t m, int64_t n, int64_t k_pad);
 cudaError_t launch_split_small(const SmallOp &a, const SmallOp &b, int s, int w,
                                unsigned int *zero_ctr, int num_sms, cudaStream_t st,
                                int *launches);

@@ -592,14 +592,12 @@ __device__ __forceinline__ int tslot(int r, int l) {
 // One 32-vector x 128-element tile of strided vectors: load (coalesced, transposed through
 // shared memory), then digits of 16 8-element chunks per row.  exps[rr] = E of vector r0+rr
 // (set and published by the caller before the call's first barrier).
-template <int W, int S, int CPX>
-__device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64_t ld,
-                                             int64_t rows, int64_t kdim, int64_t k_pad, int s,
-                                             int reverse, int conj, int8_t *__restrict__ planes,
-                                             int64_t plane_stride, int64_t per_item,
-                                             int64_t item_stride, int64_t r0, int64_t l0,
-                                             double (*tile)[128], const int32_t *exps,
-                                             uint64_t pol = 0, bool use = false) {
+template <int CPX>
+__device__ __forceinline__ void strided_tile_load(const double *__restrict__ M, int64_t ld,
+                                                  int64_t rows, int64_t kdim, int64_t per_item,
+                                                  int64_t item_stride, int64_t r0, int64_t l0,
+                                                  double (*tile)[128], uint64_t pol = 0,
+                                                  bool use = false) {
     const int tid = threadIdx.x;
     // coalesced load: warp reads 32 consecutive vectors at one l (thread: vector rr,
     // elements lg + 8 it); interior tiles take the unchecked path
@@ -638,7 +636,18 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
             for (int it = 0; it < 16; ++it) trow[tslot(rr, lg + 8 * it)] = x[it];
         }
     }
-    __syncthreads();
+}
+
+// Digits of a loaded tile (after a barrier that publishes it and exps[]).
+template <int W, int S, int CPX>
+__device__ __forceinline__ void strided_tile_digits(int64_t rows, int64_t k_pad, int s,
+                                                    int reverse, int conj,
+                                                    int8_t *__restrict__ planes,
+                                                    int64_t plane_stride, int64_t r0, int64_t l0,
+                                                    const double (*tile)[128],
+                                                    const int32_t *exps, uint64_t pol = 0,
+                                                    bool use = false) {
+    const int tid = threadIdx.x;
 #pragma unroll 1
     for (int task = tid; task < 512; task += 256) {
         const int c8 = task & 15;  // 8-element chunk of the row
@@ -673,6 +682,20 @@ __device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64
 }
 
 template <int W, int S, int CPX>
+__device__ __forceinline__ void strided_tile(const double *__restrict__ M, int64_t ld,
+                                             int64_t rows, int64_t kdim, int64_t k_pad, int s,
+                                             int reverse, int conj, int8_t *__restrict__ planes,
+                                             int64_t plane_stride, int64_t per_item,
+                                             int64_t item_stride, int64_t r0, int64_t l0,
+                                             double (*tile)[128], const int32_t *exps,
+                                             uint64_t pol = 0, bool use = false) {
+    strided_tile_load<CPX>(M, ld, rows, kdim, per_item, item_stride, r0, l0, tile, pol, use);
+    __syncthreads();
+    strided_tile_digits<W, S, CPX>(rows, k_pad, s, reverse, conj, planes, plane_stride, r0, l0,
+                                   tile, exps, pol, use);
+}
+
+template <int W, int S, int CPX>
 __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict__ M, int64_t ld,
                                                        int64_t rows, int64_t kdim, int64_t k_pad,
                                                        int s, int reverse, int conj,
@@ -704,6 +727,115 @@ __global__ void __launch_bounds__(256) k_split_strided(const double *__restrict_
     }
     strided_tile<W, S, CPX>(M, ld, rows, kdim, k_pad, s, reverse, conj, planes, plane_stride,
                             per_item, item_stride, r0, l0, tile, exps);
+}
+
+// ---------------------------------------------------------------------------------
+// Small strided operands (k_pad <= 2048): ONE launch and one read instead of the exponent-key
+// memset, the scan and the slice kernel (three dependent launches, which at 1024^2-2048^2
+// cost more than the data movement).  A cluster of CL <= 8 CTAs owns 32 vectors; CTA c loads
+// its T <= 2 tiles of 32 vectors x 128 elements (columns [c T 128, (c+1) T 128)) into shared
+// memory, computes the partial exponent key of each vector from shared memory, the CL
+// partials are combined through distributed shared memory, and each CTA converts its own tiles
+// (strided_tile_digits: the same digit code as k_split_strided).
+// ---------------------------------------------------------------------------------
+// One cluster's 32 vectors (group g) of a strided operand; c = this CTA's rank of CL; T tiles
+// of shared memory at `tiles`.  Called by every thread of every CTA of the cluster.
+template <int W, int S>
+__device__ __forceinline__ void strided_cluster_group(
+    const double *__restrict__ M, int64_t ld, int64_t rows, int64_t kdim, int64_t k_pad, int s,
+    int reverse, int8_t *__restrict__ planes, int64_t plane_stride, int32_t *__restrict__ E,
+    int64_t per_item, int64_t item_stride, int T, int64_t g, int c, int CL,
+    double (*tiles)[128], int32_t (*red)[32], int32_t *pkey, int32_t *exps) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int64_t r0 = g * 32;
+    const int64_t lb0 = (int64_t)c * T * 128;
+    const int tid = threadIdx.x;
+    for (int t = 0; t < T; ++t)
+        strided_tile_load<0>(M, ld, rows, kdim, per_item, item_stride, r0, lb0 + t * 128,
+                             tiles + 32 * t);
+    __syncthreads();
+    {  // partial key of vector rr over this CTA's columns: thread (rr, g) takes 16 of each tile
+        const int rr = tid & 31, gg = tid >> 5;
+        uint32_t mx = 0;
+        int32_t ek = kKeyEmpty;
+        for (int t = 0; t < T; ++t) {
+            const double *trow = tiles[32 * t + rr];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const double x = trow[tslot(rr, gg * 16 + j)];
+                mx = max(mx, abs_hi(x));
+                ek = max(ek, exp_key(x));
+            }
+        }
+        red[gg][rr] = key_from_hi(mx, [&]() { return ek; });
+    }
+    __syncthreads();
+    if (tid < 32) {
+        int32_t k = red[0][tid];
+#pragma unroll
+        for (int i = 1; i < 8; ++i) k = max(k, red[i][tid]);
+        pkey[tid] = k;
+    }
+    cl.sync();  // every CTA's partial keys written
+    if (tid < 32) {
+        int32_t k = kKeyEmpty;
+        for (int q = 0; q < CL; ++q) k = max(k, *cl.map_shared_rank(&pkey[tid], q));
+        const int64_t r = r0 + tid;
+        const int32_t e = r < rows ? key_to_exp(k) : 0;
+        if (c == 0 && r < rows) E[r] = e;
+        exps[tid] = e;
+    }
+    cl.sync();  // peers' partial keys read (none is overwritten or exits early); exps published
+    for (int t = 0; t < T; ++t)
+        strided_tile_digits<W, S, 0>(rows, k_pad, s, reverse, 0, planes, plane_stride, r0,
+                                     lb0 + t * 128, tiles + 32 * t, exps);
+}
+
+template <int W, int S>
+__global__ void __launch_bounds__(256) k_split_strided_cl(
+    const double *__restrict__ M, int64_t ld, int64_t rows, int64_t kdim, int64_t k_pad, int s,
+    int reverse, int8_t *__restrict__ planes, int64_t plane_stride, int32_t *__restrict__ E,
+    int64_t per_item, int64_t item_stride, int T) {
+    extern __shared__ __align__(16) double dsm[];  // T tiles [32][128] (swizzled, tslot)
+    __shared__ int32_t red[8][32];
+    __shared__ int32_t pkey[32];
+    __shared__ int32_t exps[32];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int CL = (int)cl.num_blocks();
+    strided_cluster_group<W, S>(M, ld, rows, kdim, k_pad, s, reverse, planes, plane_stride, E,
+                                per_item, item_stride, T, blockIdx.x / CL, (int)cl.block_rank(),
+                                CL, reinterpret_cast<double(*)[128]>(dsm), red, pkey, exps);
+}
+
+template <int W, int S>
+cudaError_t launch_strided_cl(const double *M, int64_t ld, int64_t rows, int64_t kdim,
+                              int64_t k_pad, int s, bool reverse, int8_t *planes,
+                              int64_t plane_stride, int32_t *E, cudaStream_t st, int *launches,
+                              BatchMap vm) {
+    const int64_t nt = ceil_div(k_pad, 128);  // 128-element tiles per vector
+    const int CL = (int)(nt < 8 ? nt : 8);
+    const int T = (int)ceil_div(nt, CL);
+    const size_t smem = (size_t)T * 32 * 128 * sizeof(double);
+    auto kern = k_split_strided_cl<W, S>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(ceil_div(rows, 32) * CL));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ++*launches;
+    return cudaLaunchKernelEx(&cfg, kern, M, ld, rows, kdim, k_pad, s, (int)reverse, planes,
+                              plane_stride, E, vm.per_item, vm.stride, T);
 }
 
 // ---------------------------------------------------------------------------------
@@ -948,246 +1080,86 @@ __global__ void __launch_bounds__(256, (W * S <= 96) ? OZ_FUSED_MINB : 1) k_spli
 }
 
 // ---------------------------------------------------------------------------------
-// Small calls (both operands together fit comfortably in L2): op(A) AND op(B) sliced in ONE
-// cooperative launch instead of 3-4 launches on two streams (exponent-key memset, scan, slice
-// on one stream, the other operand on the second, event fork / join) -- at 1024^3-2048^3 the
-// slicing phase is launch- and latency-bound, not HBM-bound.
-//  phase 1: exponent-scan tiles of both operands -- strided: 32 vectors x 512 elements (a warp
-//           reads 32 consecutive vectors at one l); contiguous: 8 vectors x 512 elements (a
-//           warp per vector) -- each writing its partial key part[ly * rows + r] (ly = l / 512),
-//           so nothing needs initialising and no atomics are used;
-//  grid-wide barrier;
-//  phase 2: digit tiles -- strided: the transposing 32 x 128 tile (strided_tile); contiguous:
-//           8 vectors x 512 elements, both 8-element chunks of a lane loaded before either is
-//           converted -- with E = max of the vector's partial keys.
-// Element arithmetic is that of the per-operand kernels (same device functions), so planes and
-// exponents are bit-identical.  Block 0 also zeroes the GEMM's wave counter, which saves the
-// GEMM launch its memset.
+// Small calls: op(A) AND op(B) sliced in ONE launch, with no memset and no second stream (the
+// default path costs the exponent-key memset, the scan and the slice of a strided operand, the
+// other operand on a second stream, an event fork / join and the wave-counter memset -- at
+// 1024^3 more latency than data movement).  Block ranges: op(A)'s blocks, then op(B)'s, each
+// a whole number of clusters of CL CTAs; a strided operand's cluster owns 32 vectors
+// (strided_cluster_group), a contiguous operand's block owns 1 or 8 vectors (contig_group).
+// Block 0 zeroes the GEMM's wave counter, and the kernel lets the GEMM (launched with
+// programmatic stream serialisation) start its set-up as soon as every block has started.
 // ---------------------------------------------------------------------------------
-// partial keys per vector: one per 512 elements (contiguous) / 128 elements (strided)
-__host__ __device__ __forceinline__ int64_t small_nls(const SmallOp &o) {
-    return o.contig ? (o.kdim + 511) / 512 : (o.kdim + 127) / 128;
-}
-__host__ __device__ __forceinline__ int64_t small_items1(const SmallOp &o) {
+__host__ __device__ __forceinline__ int64_t small_blocks(const SmallOp &o, int CL) {
     if (o.rows <= 0) return 0;
-    return (o.contig ? (o.rows + 7) / 8 : (o.rows + 31) / 32) * small_nls(o);
-}
-__host__ __device__ __forceinline__ int64_t small_items2(const SmallOp &o) {
-    if (o.rows <= 0) return 0;
-    if (o.contig) return ((o.rows + 7) / 8) * ((o.k_pad + 255) / 256);
-    return ((o.rows + 31) / 32) * ((o.k_pad + 127) / 128);
-}
-
-// Partial exponent keys of 32 strided vectors over 512 elements (tile t of operand o).
-__device__ __forceinline__ void small_scan_strided(const SmallOp &o, int64_t t, int32_t (*red)[32]) {
-    const int64_t nls = small_nls(o);
-    const int64_t rg = t / nls, ly = t - rg * nls;
-    const int64_t r0 = rg * 32, l0 = ly * 128;
-    const int tid = threadIdx.x, rr = tid & 31, lg = tid >> 5;
-    const int64_t r = r0 + rr;
-    int32_t key = kKeyEmpty;
-    if (r < o.rows) {
-        const int64_t ro = vec_off(r, 1, o.per_item, o.item_stride);
-        const double *q = o.M + ro + (l0 + lg) * o.ld;
-        const int64_t kl = o.kdim - (l0 + lg);  // elements left from this thread's first
-        const int64_t step = 8 * o.ld;
-        const bool full = kl > 8 * 15;
-        double x[16];
-#pragma unroll
-        for (int it = 0; it < 16; ++it) {
-            x[it] = (full || 8 * it < kl) ? __ldg(q) : 0.0;
-            q += step;
-        }
-        uint32_t mx = 0;
-#pragma unroll
-        for (int it = 0; it < 16; ++it) mx = max(mx, abs_hi(x[it]));
-        key = key_from_hi(mx, [&]() {  // only subnormals / zeros: exact keys
-            int32_t k2 = kKeyEmpty;
-#pragma unroll
-            for (int it = 0; it < 16; ++it) k2 = max(k2, exp_key(x[it]));
-            return k2;
-        });
-    }
-    red[lg][rr] = key;
-    __syncthreads();
-    if (tid < 32) {
-#pragma unroll
-        for (int i = 1; i < 8; ++i) key = max(key, red[i][tid]);
-        if (r < o.rows) o.part[ly * o.rows + r] = key;
-    }
-    __syncthreads();  // red[] is rewritten by the next tile
-}
-
-// Partial exponent keys of 8 contiguous vectors over 512 elements: warp wv takes vector
-// r0 + wv, lane `lane` elements l0 + 16 lane .. + 15.
-__device__ __forceinline__ void small_scan_contig(const SmallOp &o, int64_t t) {
-    const int64_t nls = small_nls(o);
-    const int64_t rg = t / nls, ly = t - rg * nls;
-    const int lane = threadIdx.x & 31;
-    const int64_t r = rg * 8 + (threadIdx.x >> 5);
-    if (r >= o.rows) return;  // warp-uniform
-    const double *v = o.M + vec_off(r, o.ld, o.per_item, o.item_stride);
-    const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
-    const int64_t l = ly * 512 + 16 * lane;
-    double x0[8], x1[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x0[i] = x1[i] = 0.0;
-    if (l < o.kdim) load8(v, l, o.kdim, al16, x0);
-    if (l + 8 < o.kdim) load8(v, l + 8, o.kdim, al16, x1);
-    uint32_t mx = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) mx = max(mx, max(abs_hi(x0[i]), abs_hi(x1[i])));
-    int32_t key = key_from_hi(mx, [&]() {
-        int32_t k2 = kKeyEmpty;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) k2 = max(k2, max(exp_key(x0[i]), exp_key(x1[i])));
-        return k2;
-    });
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o2));
-    if (lane == 0) o.part[ly * o.rows + r] = key;
-}
-
-// E of vector r from its partial keys (whole warp; every lane gets it).
-__device__ __forceinline__ int32_t small_exp_warp(const SmallOp &o, int64_t r) {
-    const int64_t nls = small_nls(o);
-    int32_t key = kKeyEmpty;
-    for (int64_t y = threadIdx.x & 31; y < nls; y += 32) key = max(key, __ldcg(o.part + y * o.rows + r));
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) key = max(key, __shfl_xor_sync(0xffffffff, key, o2));
-    return key_to_exp(key);
-}
-
-// Digits of 8 loaded elements (x is clobbered), as contig_chunk / strided_tile compute them.
-template <int W, int S>
-__device__ __forceinline__ void small_digits8(double (&x)[8], int32_t Ev, int s, int reverse,
-                                              int8_t *planes, int64_t r, int64_t lb, int64_t k_pad,
-                                              int64_t plane_stride) {
-    const bool bad = Ev == kExpNonFinite;
-    if constexpr (W * S <= 96) {
-        if (bad) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = 0.0;
-        }
-        Chunk64<W, S> c;
-        c.init(x, bad ? 0 : Ev);
-        emit64<W, S, 0>(c, s, reverse, 0, planes, r, lb, k_pad, plane_stride, 0, false);
-    } else {
-        Digits<W, S> dg[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dg[i].init(bad ? 0.0 : x[i], bad ? 0 : Ev);
-        emit<W, S, 0>(dg, s, reverse, 0, planes, r, lb, k_pad, plane_stride);
-    }
-}
-
-// Digits of 8 contiguous vectors x 256 elements (warp per vector, lane: the chunk at l0 + 8 lane,
-// i.e. 256-byte coalesced warp loads).
-template <int W, int S>
-__device__ __forceinline__ void small_digits_contig(const SmallOp &o, int64_t t, int s) {
-    const int64_t nlb = (o.k_pad + 255) / 256;
-    const int64_t rg = t / nlb, lb = t - rg * nlb;
-    const int lane = threadIdx.x & 31;
-    const int64_t r = rg * 8 + (threadIdx.x >> 5);
-    if (r >= o.rows) return;  // warp-uniform
-    const int64_t l0 = lb * 256 + 8 * lane;
-    const double *v = o.M + vec_off(r, o.ld, o.per_item, o.item_stride);
-    const bool al16 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
-    double x[8];
-    if (l0 < o.kdim) load8(v, l0, o.kdim, al16, x);  // issued before the exponent's reduction
-    const int32_t Ev = small_exp_warp(o, r);
-    if (lb == 0 && lane == 0) o.E[r] = Ev;
-    if (l0 >= o.k_pad) return;
-    if (l0 >= o.kdim) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = 0.0;
-    }
-    small_digits8<W, S>(x, Ev, s, o.reverse, o.planes, r, l0, o.k_pad, o.plane_stride);
+    const int64_t b = o.contig ? (o.k_pad >= 2048 ? o.rows : (o.rows + 7) / 8)
+                               : ((o.rows + 31) / 32) * CL;
+    return (b + CL - 1) / CL * CL;
 }
 
 template <int W, int S>
-__device__ __forceinline__ void small_digits_strided(const SmallOp &o, int64_t t, int s,
-                                                     double (*tile)[128], int32_t *exps,
-                                                     int32_t (*red)[32]) {
-    const int64_t nlb = (o.k_pad + 127) / 128, nls = small_nls(o);
-    const int64_t rg = t / nlb;
-    const int64_t r0 = rg * 32, l0 = (t - rg * nlb) * 128;
-    const int tid = threadIdx.x;
-    {  // E of the tile's 32 vectors: 8 warps reduce the partial keys, then one warp combines
-        const int rr = tid & 31, yg = tid >> 5;
-        const int64_t r = r0 + rr;
-        int32_t key = kKeyEmpty;
-        if (r < o.rows)
-            for (int64_t y = yg; y < nls; y += 8) key = max(key, __ldcg(o.part + y * o.rows + r));
-        red[yg][rr] = key;
-    }
-    __syncthreads();
-    if (tid < 32) {
-        const int64_t r = r0 + tid;
-        int32_t key = red[0][tid];
-#pragma unroll
-        for (int i = 1; i < 8; ++i) key = max(key, red[i][tid]);
-        const int32_t e = r < o.rows ? key_to_exp(key) : 0;
-        if (r < o.rows && l0 == 0) o.E[r] = e;
-        exps[tid] = e;
-    }
-    strided_tile<W, S, 0>(o.M, o.ld, o.rows, o.kdim, o.k_pad, s, o.reverse, 0, o.planes,
-                          o.plane_stride, o.per_item, o.item_stride, r0, l0, tile, exps);
-    __syncthreads();  // tile / exps are rewritten by the next tile
-}
-
-template <int W, int S>
-__global__ void __launch_bounds__(256, (S <= 13) ? 3 : 1) k_split_small(const __grid_constant__ SmallOp a,
+__global__ void __launch_bounds__(256) k_split_small(const __grid_constant__ SmallOp a,
                                                      const __grid_constant__ SmallOp b, int s,
-                                                     unsigned int *zero_ctr) {
-    __shared__ __align__(16) double tile[32][128];
+                                                     int T, unsigned int *zero_ctr) {
+    extern __shared__ __align__(16) double dsm[];  // T tiles [32][128] (strided operands)
     __shared__ int32_t red[8][32];
+    __shared__ int32_t pkey[32];
     __shared__ int32_t exps[32];
-    if (zero_ctr && blockIdx.x == 0 && threadIdx.x == 0) *zero_ctr = 0u;
-    const int64_t na = small_items1(a), nb = small_items1(b);
-    for (int64_t i = blockIdx.x; i < na + nb; i += gridDim.x) {
-        const bool ia = i < na;
-        const SmallOp &o = *(ia ? &a : &b);  // stays in the parameter space (__grid_constant__)
-        const int64_t t = ia ? i : i - na;
-        if (o.contig) small_scan_contig(o, t);
-        else small_scan_strided(o, t, red);
-    }
-    cooperative_groups::this_grid().sync();  // every partial key written and visible
-    // the GEMM (launched with programmatic stream serialisation) may start its set-up on SMs
-    // this grid leaves; it waits for this grid's completion before reading the planes
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int64_t ma = small_items2(a), mb = small_items2(b);
-    for (int64_t i = blockIdx.x; i < ma + mb; i += gridDim.x) {
-        const bool ia = i < ma;
-        const SmallOp &o = *(ia ? &a : &b);
-        const int64_t t = ia ? i : i - ma;
-        if (o.contig) small_digits_contig<W, S>(o, t, s);
-        else small_digits_strided<W, S>(o, t, s, tile, exps, red);
+    if (zero_ctr && blockIdx.x == 0 && threadIdx.x == 0) *zero_ctr = 0u;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int CL = (int)cl.num_blocks();
+    const int64_t na = small_blocks(a, CL);
+    const bool ia = (int64_t)blockIdx.x < na;
+    const SmallOp &o = *(ia ? &a : &b);  // stays in the parameter space (__grid_constant__)
+    const int64_t bi = ia ? blockIdx.x : blockIdx.x - na;
+    if (o.contig) {  // cluster-uniform: an operand spans whole clusters
+        if (o.k_pad >= 2048) {
+            if (bi < o.rows)
+                contig_group<256, W, S, 0>(o.M, o.ld, o.rows, o.kdim, o.k_pad, s, o.reverse, 0,
+                                           o.planes, o.plane_stride, o.E, o.per_item,
+                                           o.item_stride, bi, &red[0][0], 0, 0, false);
+        } else if (bi * 8 < o.rows) {
+            contig_group<32, W, S, 0>(o.M, o.ld, o.rows, o.kdim, o.k_pad, s, o.reverse, 0,
+                                      o.planes, o.plane_stride, o.E, o.per_item, o.item_stride,
+                                      bi, &red[0][0], 0, 0, false);
+        }
+        return;
     }
+    strided_cluster_group<W, S>(o.M, o.ld, o.rows, o.kdim, o.k_pad, s, o.reverse, o.planes,
+                                o.plane_stride, o.E, o.per_item, o.item_stride, T, bi / CL,
+                                (int)cl.block_rank(), CL, reinterpret_cast<double(*)[128]>(dsm),
+                                red, pkey, exps);
 }
 
 template <int W, int S>
 cudaError_t launch_small_t(const SmallOp &a, const SmallOp &b, int s, unsigned int *zero_ctr,
                            int num_sms, cudaStream_t st) {
+    (void)num_sms;
+    const int64_t nt = ceil_div(a.k_pad, 128);  // 128-element tiles per vector (same k)
+    const bool strided = !a.contig || !b.contig;
+    const int CL = strided ? (int)(nt < 8 ? nt : 8) : 1;
+    const int T = strided ? (int)ceil_div(nt, CL) : 0;
+    const size_t smem = (size_t)T * 32 * 128 * sizeof(double);
     auto kern = k_split_small<W, S>;
-    static int occ = 0;  // resident blocks per SM (per instantiation; same on every B200)
-    if (occ == 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0) != cudaSuccess ||
-            occ < 1) {
-            cudaGetLastError();
-            occ = 0;
-            return cudaErrorInvalidConfiguration;
-        }
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
     }
-    const int64_t n1 = small_items1(a) + small_items1(b);
-    const int64_t n2 = small_items2(a) + small_items2(b);
-    const int64_t need = n1 > n2 ? n1 : n2;
-    const int64_t cap = (int64_t)occ * num_sms;
-    const unsigned grid = (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
-    SmallOp a_ = a, b_ = b;
-    int s_ = s;
-    unsigned int *z_ = zero_ctr;
-    void *args[] = {&a_, &b_, &s_, &z_};
-    return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(small_blocks(a, CL) + small_blocks(b, CL)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, b, s, T, zero_ctr);
 }
 
 template <int W>
@@ -1327,6 +1299,17 @@ cudaError_t launch_split_t(const double *M, int64_t ld, bool contiguous, int64_t
     if (fused) return launch_fused<W, S, CPX, false>(M, ld, rows, kdim, k_pad, s, reverse, conj,
                                                       planes, plane_stride, E, key_scratch,
                                                       num_sms, st, launches, vm);
+    // small real operands (k_pad <= 1024, <= OZIMMU_SPLIT_CL_MB of input, default 64): one
+    // clustered launch (k_split_strided_cl) instead of memset + scan + slice (1024^2: 18.5 ->
+    // 10 us of kernel time, cold; at k_pad = 2048 two tiles per CTA made it slower: 29.7 ->
+    // 32.8 us)
+    if constexpr (CPX == 0) {
+        static const int64_t cl_mb =
+            getenv("OZIMMU_SPLIT_CL_MB") ? atoi(getenv("OZIMMU_SPLIT_CL_MB")) : 64;
+        if (k_pad <= 1024 && rows * kdim * 8 <= (cl_mb << 20))
+            return launch_strided_cl<W, S>(M, ld, rows, kdim, k_pad, s, reverse, planes,
+                                           plane_stride, E, st, launches, vm);
+    }
     cudaError_t e = launch_expscan(M, ld, rows, CPX ? kdim / 2 : kdim, key_scratch, num_sms, st,
                                    launches, CPX ? 1 : 0, vm);
     if (e != cudaSuccess) return e;
@@ -1398,23 +1381,16 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
     }
 }
 
-// Both operands of a small call in one launch (see k_split_small).
-size_t split_small_part_bytes(int64_t m, int64_t n, int64_t k_pad) {
-    if (!split_small_ok(m, n, k_pad)) return 0;
-    // one partial key per 128 elements (strided) or 512 (contiguous) of each vector
-    return sizeof(int32_t) * (size_t)((k_pad + 127) / 128) * (size_t)(m + n);
-}
-
+// Both operands of a small call in one launch (see k_split_small): real operands whose input
+// bytes sum to at most OZIMMU_SPLIT_SMALL_MB (default 80; 0 disables) and k_pad <= 1024 (one
+// 32 x 128 tile per CTA of a strided operand's cluster).  Measured: 1024^3
+// call 80.4 -> 77.1 us; with k_pad = 1536-2048 (two tiles, 64 KB of shared memory for every
+// block of the launch) slower than the per-operand kernels (2048^3 313 -> 320 us).
 bool split_small_ok(int64_t m, int64_t n, int64_t k_pad) {
-    // sum of both operands' input bytes <= OZIMMU_SPLIT_SMALL_MB.  Off by default (0): measured
-    // slower than the per-operand kernels on two streams (1024^3 slicing 21 -> 25
-    // us, 2048^3 45 -> 62 us) -- with ~3 resident blocks per SM each block walks its work items
-    // in rounds of dependent memory round trips, where the per-operand launches have every item
-    // in flight at once
     static const int64_t lim =
-        (int64_t)(getenv("OZIMMU_SPLIT_SMALL_MB") ? atoi(getenv("OZIMMU_SPLIT_SMALL_MB")) : 0)
+        (int64_t)(getenv("OZIMMU_SPLIT_SMALL_MB") ? atoi(getenv("OZIMMU_SPLIT_SMALL_MB")) : 80)
         << 20;
-    return m > 0 && n > 0 && (m + n) * k_pad * 8 <= lim;
+    return m > 0 && n > 0 && k_pad <= 1024 && (m + n) * k_pad * 8 <= lim;
 }
 
 cudaError_t launch_split_small(const SmallOp &a, const SmallOp &b, int s, int w,

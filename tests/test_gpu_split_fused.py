@@ -2,8 +2,9 @@
 panel in one persistent launch, slice tiles waiting on their panel's scan tiles; SplitInt,
 Alg. 4, readings A3-A5/A11).  Children run with the fused kernel at its default
 panel size, with tiny panels (many panels, ragged last panel, scans and slices of different
-panels interleaved) and with the two-launch path (OZIMMU_SPLIT_FUSED=0); the DGEMMs also run
-with both operands sliced in one cooperative launch (k_split_small, OZIMMU_SPLIT_SMALL_MB); the
+panels interleaved) and with the per-operand kernels (OZIMMU_SPLIT_FUSED=0,
+OZIMMU_SPLIT_SMALL_MB=0, the base); the DGEMMs also run with both operands sliced in one
+clustered launch (k_split_small, the default for small calls, here also up to 512 MB); the
 GEMM cases also
 run with one TMEM accumulator instead of two (OZIMMU_ACC2=0).  Planes, exponents and C must
 be bitwise equal across the variants and to the CPU oracle."""
@@ -23,12 +24,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from split_child import DGEMMS, SPLITS, ZGEMMS, split_matrix  # noqa: E402
 
-VARIANTS = {"two_launch": {"OZIMMU_SPLIT_FUSED": "0"},
+VARIANTS = {"two_launch": {"OZIMMU_SPLIT_FUSED": "0", "OZIMMU_SPLIT_SMALL_MB": "0"},
+            "default": {},
             "fused": {"OZIMMU_SPLIT_FUSED": "1"},
             "fused_small_panels": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_PANEL_KB": "24"},
             "fused_bps2": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_FUSED_BPS": "2"},
-            # both operands of a DGEMM in one cooperative launch (k_split_small, opt-in)
+            # both operands of a DGEMM in one launch (k_split_small) up to 512 MB of input
             "small_one_launch": {"OZIMMU_SPLIT_SMALL_MB": "512"},
+            # small strided operands: scan + slice kernels instead of the clustered one-launch
+            # kernel (k_split_strided_cl, the default for k_pad <= 2048)
+            "no_cluster_split": {"OZIMMU_SPLIT_CL_MB": "0"},
             # GEMM side: one TMEM accumulator buffer instead of two for short K (s <= 8)
             "one_acc": {"OZIMMU_ACC2": "0"}}
 
