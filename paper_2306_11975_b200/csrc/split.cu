@@ -1138,10 +1138,18 @@ cudaError_t launch_small_t(const SmallOp &a, const SmallOp &b, int s, unsigned i
     (void)num_sms;
     const int64_t nt = ceil_div(a.k_pad, 128);  // 128-element tiles per vector (same k)
     const bool strided = !a.contig || !b.contig;
-    const int CL = strided ? (int)(nt < 8 ? nt : 8) : 1;
+    // one 32 x 128 tile per CTA: clusters of up to 16 CTAs (16 = the non-portable maximum, for
+    // 1024 < k_pad <= 2048), so every block of the launch reserves 32 KB of shared memory
+    static const int max_cl =
+        getenv("OZIMMU_SPLIT_SMALL_CL") ? atoi(getenv("OZIMMU_SPLIT_SMALL_CL")) : 16;
+    const int CL = strided ? (int)(nt < max_cl ? nt : max_cl) : 1;
     const int T = strided ? (int)ceil_div(nt, CL) : 0;
     const size_t smem = (size_t)T * 32 * 128 * sizeof(double);
     auto kern = k_split_small<W, S>;
+    if (CL > 8) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -1385,12 +1393,16 @@ cudaError_t launch_split(const double *M, int64_t ld, bool contiguous, int64_t r
 // bytes sum to at most OZIMMU_SPLIT_SMALL_MB (default 80; 0 disables) and k_pad <= 1024 (one
 // 32 x 128 tile per CTA of a strided operand's cluster).  Measured: 1024^3
 // call 80.4 -> 77.1 us; with k_pad = 1536-2048 (two tiles, 64 KB of shared memory for every
-// block of the launch) slower than the per-operand kernels (2048^3 313 -> 320 us).
+// block of the launch) slower than the per-operand kernels (2048^3 313 -> 320 us), and so with
+// one tile per CTA in clusters of up to 16 (2048^3 310 -> 325 us; OZIMMU_SPLIT_SMALL_K raises
+// the k_pad limit for experiments).
 bool split_small_ok(int64_t m, int64_t n, int64_t k_pad) {
     static const int64_t lim =
         (int64_t)(getenv("OZIMMU_SPLIT_SMALL_MB") ? atoi(getenv("OZIMMU_SPLIT_SMALL_MB")) : 80)
         << 20;
-    return m > 0 && n > 0 && k_pad <= 1024 && (m + n) * k_pad * 8 <= lim;
+    static const int64_t kmax =
+        getenv("OZIMMU_SPLIT_SMALL_K") ? atoi(getenv("OZIMMU_SPLIT_SMALL_K")) : 1024;
+    return m > 0 && n > 0 && k_pad <= kmax && (m + n) * k_pad * 8 <= lim;
 }
 
 cudaError_t launch_split_small(const SmallOp &a, const SmallOp &b, int s, int w,

@@ -27,7 +27,9 @@ DGEMMS = [("N", "N", 300, 200, 5000, 9), ("T", "T", 129, 300, 2500, 13),
           # k > 2^17: w = 6 digits
           ("N", "T", 24, 40, 140000, 9),
           # op(A) strided, ~1000 rows
-          ("N", "N", 1300, 64, 1200, 9)]
+          ("N", "N", 1300, 64, 1200, 9),
+          # both operands strided, 1024 < k_pad <= 2048: clusters of 15 CTAs in the small path
+          ("N", "T", 200, 150, 1800, 9)]
 # zgemm: (ta, tb, m, n, k, s)
 ZGEMMS = [("N", "N", 200, 96, 1500, 9), ("C", "T", 70, 45, 1100, 12), ("T", "C", 65, 33, 2100, 8),
           ("N", "T", 3000, 64, 256, 8)]

@@ -29,8 +29,9 @@ VARIANTS = {"two_launch": {"OZIMMU_SPLIT_FUSED": "0", "OZIMMU_SPLIT_SMALL_MB": "
             "fused": {"OZIMMU_SPLIT_FUSED": "1"},
             "fused_small_panels": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_PANEL_KB": "24"},
             "fused_bps2": {"OZIMMU_SPLIT_FUSED": "1", "OZIMMU_SPLIT_FUSED_BPS": "2"},
-            # both operands of a DGEMM in one launch (k_split_small) up to 512 MB of input
-            "small_one_launch": {"OZIMMU_SPLIT_SMALL_MB": "512"},
+            # both operands of a DGEMM in one launch (k_split_small) up to 512 MB of input and
+            # k_pad <= 2048 (clusters of up to 16 CTAs)
+            "small_one_launch": {"OZIMMU_SPLIT_SMALL_MB": "512", "OZIMMU_SPLIT_SMALL_K": "2048"},
             # small strided operands: scan + slice kernels instead of the clustered one-launch
             # kernel (k_split_strided_cl, the default for k_pad <= 2048)
             "no_cluster_split": {"OZIMMU_SPLIT_CL_MB": "0"},
