@@ -163,13 +163,16 @@ def cpu_baseline_sample(A, B, k, s, target_s=15.0):
     m, n = A.shape[0], B.shape[1]
     rng = np.random.default_rng(7)
     # calibrate on a tiny block, then size the sample for ~target_s of CPU work
-    r0 = rng.choice(m, 8, replace=False)
-    c0 = rng.choice(n, 32, replace=False)
+    # (16 x 256 outputs: enough work per call for the oracle's threads; an 8 x 32 block
+    # overestimated the per-output cost about 4x, so the sample ran ~4 s instead of ~15 s)
+    cr, cc = min(m, 16), min(n, 256)
+    r0 = rng.choice(m, cr, replace=False)
+    c0 = rng.choice(n, cc, replace=False)
     t = time.perf_counter()
-    O.dgemm("N", "N", 8, 32, k, 1.0, np.asfortranarray(A[r0]), 8, np.asfortranarray(B[:, c0]),
-            k, 0.0, np.zeros((8, 32), order="F"), 8, s)
+    O.dgemm("N", "N", cr, cc, k, 1.0, np.asfortranarray(A[r0]), cr, np.asfortranarray(B[:, c0]),
+            k, 0.0, np.zeros((cr, cc), order="F"), cr, s)
     dt = max(time.perf_counter() - t, 1e-3)
-    per_elem = dt / (8 * 32)
+    per_elem = dt / (cr * cc)
     nel = max(256, int(target_s / per_elem))
     rows_n = int(min(m, max(8, 2 ** int(np.log2(max(8, np.sqrt(nel / 8)))))))
     cols_n = int(min(n, max(32, nel // rows_n)))
